@@ -1,0 +1,172 @@
+/*
+ * headinfer.h -- C ABI of libheadinfer.so, the B200-native hot path of HeadInfer
+ * (arXiv 2502.12574): causal GQA attention computed one KV head at a time, with
+ * every head's K/V cache held in NUMA-local pinned host RAM and streamed to the
+ * GPU through ping-pong staging slots.
+ *
+ * Citations: "P:Lnnn" = /root/reference/PAPER.md line nnn (section / equation /
+ * algorithm named alongside); SURVEY.md §8(b) fixes names and argument order.
+ *
+ * General conventions (apply to every call below)
+ *  - Types: all tensors are bf16 (IEEE bfloat16 bit patterns), row-major, dense.
+ *  - Head sharding: a context created with (rank, world) owns the
+ *    kv heads [rank*kv_heads/world, (rank+1)*kv_heads/world) and the matching q heads
+ *    [rank*q_heads/world, (rank+1)*q_heads/world).  Hkv_loc = kv_heads/world,
+ *    Hq_loc = q_heads/world, g = q_heads/kv_heads.  "Local" head indices start at 0.
+ *  - GQA (reading R4): local q head j reads local kv head floor(j/g).
+ *  - Ownership: the caller owns Q/K/V/out (device pointers on the context's device,
+ *    16-byte aligned).  The library owns the host KV store and all device staging and
+ *    workspaces, and never retains caller pointers after a call returns.  Every call
+ *    is stream-ordered on `cuda_stream` (a cudaStream_t; NULL = legacy default
+ *    stream): the library's internal streams wait for the caller's prior work, and
+ *    the caller's stream is made to wait for every internal operation that reads a
+ *    caller input or writes `out`, so buffers may be reused/freed in stream order.
+ *    Calls return as soon as the work is enqueued (no host synchronisation).
+ *  - Errors: return codes only, never an abort or exception across the ABI.  Argument
+ *    validation happens before any state change (a failed call leaves the context
+ *    untouched).  A CUDA error poisons the context ("sticky"): every later call
+ *    except hi_free / hi_status_str / hi_last_error returns HI_ECUDA.
+ *  - Threading: one host thread per context at a time.  No CPU fallback exists: on a
+ *    machine without a usable CUDA device hi_init returns HI_ECUDA.
+ */
+#ifndef HEADINFER_H_
+#define HEADINFER_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hi_ctx hi_ctx; /* opaque; one per (process, GPU) */
+
+typedef enum {
+    HI_OK = 0,
+    HI_EINVAL = 1,      /* bad configuration: sizes <= 0, q_heads % kv_heads, kv_heads % world, head_dim not 64/128 */
+    HI_ESHAPE = 2,      /* bad call shape: layer out of range, n_tokens < 1 or > chunk, NULL pointer */
+    HI_ECAPACITY = 3,   /* seq_len[layer] + n would exceed max_ctx ("CapacityExceeded") */
+    HI_ENOMEM_HOST = 4, /* host KV store could not be allocated / pinned */
+    HI_ENOMEM_DEV = 5,  /* device staging / workspace allocation failed */
+    HI_ECUDA = 6,       /* CUDA runtime error (context is now sticky-failed) */
+    HI_ESTATE = 7       /* call not valid in the current state */
+} hi_status;
+
+/* Advanced options for hi_init_ex (tests and benches); zero-initialise, then set fields.
+ * Any field left 0 takes the default shown. */
+typedef struct hi_options {
+    int n_slots;          /* staging slots per context (default 4, min 2: "ping-pong", Fig. 4) */
+    int64_t slot_tokens;  /* tokens per slot (default floor(max_ctx/n_slots) rounded down to 64, min 64),
+                             so that n_slots*slot_tokens*4*head_dim <= one head's K+V at max_ctx (Eq. 11) */
+    int device;           /* CUDA device ordinal (default: the current device) */
+    int flags;            /* HI_FLAG_* bits */
+    int numa_policy;      /* 0 = bind the host store to the GPU's NUMA node (sysfs), 1 = no binding,
+                             2 = bind to numa_node */
+    int numa_node;        /* used when numa_policy == 2 */
+} hi_options;
+
+#define HI_FLAG_POISON_SLOTS 0x1 /* fill each staging slot with NaN before every H2D (race detection) */
+#define HI_FLAG_NO_HUGEPAGE 0x2  /* do not madvise(MADV_HUGEPAGE) the host store */
+#define HI_FLAG_SERIALIZE 0x4    /* synchronise after every internal step (debug; destroys overlap) */
+
+typedef struct hi_stats {
+    int64_t host_store_bytes;     /* pinned host KV bytes (L * Hkv_loc * max_ctx * 4 * d) */
+    int64_t staging_bytes;        /* device staging slots, total */
+    int64_t staging_bound_bytes;  /* one head at max_ctx: 4*d*max_ctx (Eq. 11, reading R8) */
+    int64_t workspace_bytes;      /* other device buffers (pack, accumulators, partials) */
+    int64_t h2d_bytes;            /* cumulative history bytes streamed host->device */
+    int64_t d2h_bytes;            /* cumulative new-K/V bytes written back device->host */
+    int64_t prefill_calls, decode_calls;
+    int64_t kernel_launches;      /* cumulative launches of this library's kernels */
+    double init_seconds;          /* wall time of hi_init (host pinning dominates) */
+    int numa_node;                /* node the host store is bound to (-1: none / unknown) */
+    int n_slots;
+    int64_t slot_tokens;
+} hi_stats;
+
+/*
+ * hi_init -- pre-allocate everything (Alg. 1 lines 1-2; "pre-allocates the
+ * CPU's KV cache memory and the GPU's ping-pong memory", §4).
+ *   layers, q_heads, kv_heads, head_dim: model shape (head_dim in {64,128}).
+ *   max_ctx: tokens per (layer, kv head) the host store holds (Eq. 4 P:L169 sizes it).
+ *   chunk:   largest n_tokens a hi_prefill_chunk call may pass (§3.3 chunked prefill).
+ *   rank, world: head shard (see conventions).  *out receives the handle (NULL on failure).
+ * Host store: one contiguous K region and one V region of max_ctx*head_dim bf16 per
+ * (layer, local kv head) (Eq. 7-8: "each head stores its keys and values in a
+ * contiguous memory space"), mmap'd, bound to the GPU's NUMA node, pinned.
+ * Errors: HI_EINVAL, HI_ENOMEM_HOST, HI_ENOMEM_DEV, HI_ECUDA (e.g. no GPU).
+ */
+hi_status hi_init(int layers, int q_heads, int kv_heads, int head_dim, int64_t max_ctx, int chunk,
+                  int rank, int world, hi_ctx** out);
+hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_t max_ctx, int chunk,
+                     int rank, int world, const hi_options* opt, hi_ctx** out);
+
+/*
+ * hi_prefill_chunk -- one chunk of the prefill phase for one layer (Alg. 1 lines 3-17,
+ * P:L316-333): for every local kv head h, write the chunk's K/V of head h back to host
+ * rows [s, s+n) (line 11 "Async Update CPU KV cache", delta write-back, reading R7),
+ * stream head h's history rows [0, s) in through the staging slots (line 10 "Async
+ * Prefetch"), and compute causal attention (line 13, Eq. 9) for the g q heads of
+ * the group over history + chunk; outputs land in their q-head columns of `out`
+ * (line 15 "Concatenate").  s = hi_seq_len(layer) before the call; it advances by n.
+ *   Q   [n_tokens, Hq_loc, head_dim]   bf16 device, q heads of this shard, global positions s..s+n-1
+ *   K,V [n_tokens, Hkv_loc, head_dim]  bf16 device
+ *   out [n_tokens, Hq_loc, head_dim]   bf16 device (written)
+ *   n_tokens in [1, chunk]; the last chunk may be partial (reading R11).
+ * Errors: HI_ESHAPE, HI_ECAPACITY, HI_ECUDA, HI_ESTATE.
+ */
+hi_status hi_prefill_chunk(hi_ctx* ctx, int layer, const void* Q, const void* K, const void* V, void* out,
+                           int n_tokens, void* cuda_stream);
+
+/*
+ * hi_decode -- one generated token for one layer (Alg. 1 lines 18-32): append
+ * k, v at position s (host row s, D2H) and attend q to keys 0..s, the new key included
+ * (reading R3), streaming each head's history [0, s) through the slots; split-K partials
+ * merged by log-sum-exp.  s advances by 1.  s = 0 is allowed (out = v).
+ *   q [Hq_loc, head_dim], k, v [Hkv_loc, head_dim], out [Hq_loc, head_dim]: bf16 device.
+ * Errors: HI_ESHAPE, HI_ECAPACITY, HI_ECUDA, HI_ESTATE.
+ */
+hi_status hi_decode(hi_ctx* ctx, int layer, const void* q, const void* k, const void* v, void* out,
+                    void* cuda_stream);
+
+/* hi_free -- synchronise, unpin and release everything.  NULL is a no-op (HI_OK). */
+hi_status hi_free(hi_ctx* ctx);
+
+/* ---- verification / introspection / bench preparation (not on the hot path) ---- */
+
+/* Copy host KV rows [pos, pos+n) of (layer, local kv head) into host buffers k_dst, v_dst
+ * ([n, head_dim] bf16 each).  Waits for pending write-backs first.  HI_ESHAPE on bad range. */
+hi_status hi_read_host_kv(hi_ctx* ctx, int layer, int kv_head_local, int64_t pos, int64_t n,
+                          void* k_dst, void* v_dst);
+
+/* Write host KV rows [pos, pos+n) of (layer, local kv head) from k_src, v_src ([n, head_dim]
+ * bf16 each; device pointers if from_device != 0, else host).  Synchronous.  Does not move
+ * seq_len.  This is the "helper for simulating or preparing decoding with large context"
+ * (App. E): benches fill a long history without timing a full prefill. */
+hi_status hi_write_host_kv(hi_ctx* ctx, int layer, int kv_head_local, int64_t pos, int64_t n,
+                           const void* k_src, const void* v_src, int from_device);
+
+/* seq_len[layer]: tokens cached for `layer` (all local kv heads share it).  -1 on bad args. */
+int64_t hi_seq_len(const hi_ctx* ctx, int layer);
+
+/* Set seq_len[layer] = s (0 <= s <= max_ctx).  Rows below s are taken as valid history;
+ * used to rewind a bench to an earlier position (host history is immutable, so re-running
+ * a chunk rewrites identical bytes).  Waits for in-flight work of the context. */
+hi_status hi_set_seq_len(hi_ctx* ctx, int layer, int64_t s);
+
+/* Snapshot of counters; waits for in-flight work of the context. */
+hi_status hi_get_stats(hi_ctx* ctx, hi_stats* out);
+
+/* Blocks until all work the context enqueued has finished. */
+hi_status hi_synchronize(hi_ctx* ctx);
+
+const char* hi_status_str(hi_status s);
+
+/* Message describing the last failure on this context (or of the last failed hi_init when
+ * ctx is NULL).  Never NULL. */
+const char* hi_last_error(const hi_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HEADINFER_H_ */

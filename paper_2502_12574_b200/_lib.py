@@ -1,0 +1,82 @@
+"""ctypes loader for libheadinfer.so (the C ABI declared in include/headinfer.h).
+
+Fails loudly when the native library is missing: there is no CPU or eager fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libheadinfer.so")
+
+HI_OK, HI_EINVAL, HI_ESHAPE, HI_ECAPACITY, HI_ENOMEM_HOST, HI_ENOMEM_DEV, HI_ECUDA, HI_ESTATE = range(8)
+STATUS_NAMES = ["HI_OK", "HI_EINVAL", "HI_ESHAPE", "HI_ECAPACITY", "HI_ENOMEM_HOST", "HI_ENOMEM_DEV",
+                "HI_ECUDA", "HI_ESTATE"]
+HI_FLAG_POISON_SLOTS = 0x1
+HI_FLAG_NO_HUGEPAGE = 0x2
+HI_FLAG_SERIALIZE = 0x4
+
+# every symbol include/headinfer.h declares (checked by tests/test_abi.py)
+EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",
+           "hi_write_host_kv", "hi_seq_len", "hi_set_seq_len", "hi_get_stats", "hi_synchronize",
+           "hi_status_str", "hi_last_error"]
+
+
+class hi_options(ctypes.Structure):
+    _fields_ = [("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64), ("device", ctypes.c_int),
+                ("flags", ctypes.c_int), ("numa_policy", ctypes.c_int), ("numa_node", ctypes.c_int)]
+
+
+class hi_stats(ctypes.Structure):
+    _fields_ = [("host_store_bytes", ctypes.c_int64), ("staging_bytes", ctypes.c_int64),
+                ("staging_bound_bytes", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("prefill_calls", ctypes.c_int64), ("decode_calls", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64), ("init_seconds", ctypes.c_double),
+                ("numa_node", ctypes.c_int), ("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libheadinfer.so (raises if it was not built -- run __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2502_12574_b200.build` "
+                           "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, I64, VP = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+    lib.hi_init.argtypes = [I, I, I, I, I64, I, I, I, ctypes.POINTER(P)]
+    lib.hi_init_ex.argtypes = [I, I, I, I, I64, I, I, I, ctypes.POINTER(hi_options), ctypes.POINTER(P)]
+    lib.hi_prefill_chunk.argtypes = [P, I, VP, VP, VP, VP, I, VP]
+    lib.hi_decode.argtypes = [P, I, VP, VP, VP, VP, VP]
+    lib.hi_free.argtypes = [P]
+    lib.hi_read_host_kv.argtypes = [P, I, I, I64, I64, VP, VP]
+    lib.hi_write_host_kv.argtypes = [P, I, I, I64, I64, VP, VP, I]
+    lib.hi_seq_len.argtypes = [P, I]
+    lib.hi_seq_len.restype = I64
+    lib.hi_set_seq_len.argtypes = [P, I, I64]
+    lib.hi_get_stats.argtypes = [P, ctypes.POINTER(hi_stats)]
+    lib.hi_synchronize.argtypes = [P]
+    lib.hi_status_str.argtypes = [I]
+    lib.hi_status_str.restype = ctypes.c_char_p
+    lib.hi_last_error.argtypes = [P]
+    lib.hi_last_error.restype = ctypes.c_char_p
+    for name in ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",
+                 "hi_write_host_kv", "hi_set_seq_len", "hi_get_stats", "hi_synchronize"]:
+        getattr(lib, name).restype = I
+    _lib = lib
+    return lib
+
+
+class HIError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 8 else status}: {msg}")

@@ -1,0 +1,71 @@
+"""Build the native libraries in-tree for sm_100a (B200).
+
+    python -m paper_2502_12574_b200.build      # or __graft_entry__.build()
+
+Outputs
+  paper_2502_12574_b200/libheadinfer.so   -- the C ABI (include/headinfer.h) + kernels
+  synth/libsynth.so                       -- seeded input generator twin (test/bench infra)
+cudart is linked statically (nvcc default), so the libraries load on a GPU-less host too.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2502_12574_b200")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr"]
+
+
+def _stale(out: str, srcs) -> bool:
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(s) > t for s in srcs)
+
+
+def _nvcc_shared(out: str, srcs, extra=(), force=False, verbose=False):
+    deps = list(srcs) + glob.glob(os.path.join(os.path.dirname(srcs[0]), "*.cuh")) + \
+        glob.glob(os.path.join(ROOT, "include", "*.h"))
+    if not force and not _stale(out, deps):
+        return out
+    objs = []
+    bdir = os.path.join(os.path.dirname(out), "build")
+    os.makedirs(bdir, exist_ok=True)
+    procs = []
+    for s in srcs:
+        o = os.path.join(bdir, os.path.basename(s) + ".o")
+        cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", s, "-o", o]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), s))
+        objs.append(o)
+    failed = False
+    for p, s in procs:
+        outp = p.communicate()[0].decode()
+        if p.returncode != 0:
+            sys.stderr.write(f"nvcc failed for {s}:\n{outp}\n")
+            failed = True
+        elif verbose and outp:
+            sys.stderr.write(outp)
+    if failed:
+        raise RuntimeError("nvcc compilation failed")
+    tmp = out + f".tmp{os.getpid()}"
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"])
+    os.replace(tmp, out)
+    return out
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
+    _nvcc_shared(os.path.join(PKG, "libheadinfer.so"), srcs, force=force, verbose=verbose)
+    ssrc = sorted(glob.glob(os.path.join(ROOT, "synth", "csrc", "*.cu")))
+    _nvcc_shared(os.path.join(ROOT, "synth", "libsynth.so"), ssrc, force=force, verbose=verbose)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)

@@ -1,0 +1,72 @@
+// hi_kernels.cuh -- internal launch interface between the host runtime (hi_runtime.cu)
+// and the device kernels of libheadinfer.so.  Not part of the public ABI.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hi {
+
+// ---- prefill attention over one KV segment -------------------------
+// Computes, for the g q heads of one kv head group, rows r = t*g + j (token t of the chunk,
+// group member j; GQA packing), the flash-attention update of the running state
+// (O, m, l) with the keys of ONE contiguous segment [k_pos0, k_pos0 + n_k): either a history
+// block sitting in a staging slot or the chunk's own K/V (causal).  Scores are kept in the
+// log2 domain: x = (q.k) * log2(e)/sqrt(d); m is the running max of x, l = sum 2^(x-m),
+// O = sum 2^(x-m) v.  FIRST initialises the state, LAST writes out = O / l as bf16.
+enum PrefillFlags : int { PF_FIRST = 1, PF_LAST = 2, PF_CAUSAL = 4 };
+
+struct PrefillParams {
+    const __nv_bfloat16* q;   // (token 0, first q head of the group); row (t,j) at q + t*q_tok_stride + j*d
+    int64_t q_tok_stride;     // elements between consecutive tokens (Hq_loc * d)
+    __nv_bfloat16* out;       // same addressing as q
+    int64_t o_tok_stride;
+    const __nv_bfloat16* k;   // key i of the segment at k + i*kv_row_stride
+    const __nv_bfloat16* v;
+    int64_t kv_row_stride;
+    int n_q;                  // tokens in the chunk
+    int n_k;                  // keys in this segment
+    int64_t q_pos0;           // global position of token 0
+    int64_t k_pos0;           // global position of key 0 of the segment
+    int g;                    // q heads per kv head
+    float scale_log2;         // log2(e) / sqrt(d)
+    float* o_acc;             // [n_q*g][d] fp32 running O
+    float* m_acc;             // [n_q*g]
+    float* l_acc;             // [n_q*g]
+    int flags;
+};
+cudaError_t launch_prefill(const PrefillParams& p, int d, cudaStream_t stream);
+
+// ---- decode: split-K partials over one history block + LSE combine (a8) ----------------
+struct DecodePartialParams {
+    const __nv_bfloat16* q;   // [g][d] q rows of the group (contiguous)
+    const __nv_bfloat16* k;   // [n_k][d] block in a staging slot
+    const __nv_bfloat16* v;
+    int n_k;
+    int split_len;            // keys per CTA
+    float scale_log2;
+    float* parts;             // records for this launch: parts + (blockIdx.x*g + j)*(d+4): {m, l, pad, pad, o[d]}
+};
+cudaError_t launch_decode_partial(const DecodePartialParams& p, int d, int g, int n_splits, cudaStream_t stream);
+
+struct DecodeCombineParams {
+    const __nv_bfloat16* q;      // [Hq_loc][d]
+    const __nv_bfloat16* k_new;  // [Hkv_loc][d]  the new token's key (attends itself, reading R3)
+    const __nv_bfloat16* v_new;  // [Hkv_loc][d]
+    const float* parts;          // [Hkv_loc][max_parts][g][d+4]
+    int max_parts;
+    int n_parts;                 // parts per kv head filled by this call (same for every head)
+    int g;
+    float scale_log2;
+    __nv_bfloat16* out;          // [Hq_loc][d]
+};
+cudaError_t launch_decode_combine(const DecodeCombineParams& p, int d, int hq_loc, cudaStream_t stream);
+
+// ---- pack the chunk's K and V [n][Hkv][d] into head-major [Hkv][2][n][d] (a2, K5b) ------
+cudaError_t launch_pack_kv(const __nv_bfloat16* k, const __nv_bfloat16* v, __nv_bfloat16* packed,
+                           int n, int hkv, int d, cudaStream_t stream);
+
+// ---- fill with a NaN bit pattern (poison mode, race detection) --------------------------
+cudaError_t launch_poison(void* ptr, size_t bytes, cudaStream_t stream);
+
+}  // namespace hi

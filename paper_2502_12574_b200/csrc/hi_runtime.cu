@@ -1,0 +1,644 @@
+// hi_runtime.cu -- host runtime of libheadinfer.so: the C ABI declared in include/headinfer.h.
+//
+// Subsystems (SURVEY.md §1 "The build", 2(a)-(f)):
+//  (a) host KV store   -- one contiguous K and V region per (layer, local kv head) (Eq. 7-8,
+//                         P:L203-213), mmap'd, NUMA-bound to the GPU's node, first-touched in
+//                         parallel, pinned with cudaHostRegister (pre-allocation, §4).
+//  (b) staging pool    -- n_slots device slots, each [slot_tokens][d] K + [slot_tokens][d] V,
+//                         n_slots*slot_tokens <= max_ctx: at most one head's K/V resident
+//                         (Eq. 10-11; the ping-pong memory of Fig. 4).
+//  (c) copy engine     -- dedicated H2D and D2H streams; every slot hand-off is an event
+//                         (slot_ready: H2D -> compute, slot_free: compute -> H2D), so H2D of
+//                         head h+1, D2H of the chunk and compute on head h run concurrently,
+//                         full duplex (§4; App. D).
+//  (d) scheduler       -- per call: pack + write-back, then per kv head the chunk's own
+//                         (causal) segment first -- it needs no transfer -- followed by the
+//                         history blocks in landing order; the host only enqueues (never
+//                         blocks), so the copy stream runs ahead across heads and layers.
+//  (e) kernels         -- k_prefill_*.cu, k_decode.cu, k_pack.cu.
+//  (f) stats + errors  -- status codes, sticky CUDA failure, hi_stats counters.
+#include "../../include/headinfer.h"
+#include "hi_kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <linux/mempolicy.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_init_error = "no error";
+
+struct Slot {
+    cudaEvent_t ready = nullptr;  // recorded on the H2D stream after the block landed
+    cudaEvent_t free_ = nullptr;  // recorded on the compute stream after its consumer kernel
+};
+
+}  // namespace
+
+struct hi_ctx {
+    // configuration
+    int L = 0, Hq = 0, Hkv = 0, d = 0, chunk = 0, rank = 0, world = 1;
+    int Hq_loc = 0, Hkv_loc = 0, g = 0, device = 0, flags = 0;
+    int64_t max_ctx = 0;
+    float scale_log2 = 0.f;
+    // state
+    std::vector<int64_t> seq_len;
+    bool sticky = false;
+    std::string err = "no error";
+    // (a) host KV store
+    uint8_t* host = nullptr;
+    size_t host_bytes = 0;
+    size_t host_map_bytes = 0;
+    bool host_registered = false;
+    int numa_node = -1;
+    // (b) staging
+    int n_slots = 0;
+    int64_t slot_tokens = 0;
+    size_t slot_bytes = 0;
+    uint8_t* d_stage = nullptr;
+    std::vector<Slot> slots;
+    int next_slot = 0;
+    // (c) streams + events
+    cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_call_in = nullptr, ev_call_out = nullptr, ev_packed = nullptr, ev_pack_free = nullptr;
+    std::vector<cudaEvent_t> ev_layer_d2h;   // last write-back of each layer's rows
+    std::vector<cudaEvent_t> ev_kvnew_free;  // decode: kvnew[layer] read by its D2H
+    // workspaces
+    __nv_bfloat16* d_pack = nullptr;   // [Hkv_loc][2][chunk][d]
+    float* d_oacc = nullptr;           // [chunk*g][d]
+    float* d_macc = nullptr;           // [chunk*g]
+    float* d_lacc = nullptr;           // [chunk*g]
+    float* d_parts = nullptr;          // [Hkv_loc][max_parts][g][d+4]
+    int max_parts = 0;
+    __nv_bfloat16* d_kvnew = nullptr;  // [L][2][Hkv_loc][d]
+    size_t workspace_bytes = 0;
+    // (f) stats
+    int64_t h2d_bytes = 0, d2h_bytes = 0, prefill_calls = 0, decode_calls = 0, launches = 0;
+    double init_seconds = 0.0;
+
+    uint8_t* host_k(int layer, int h, int64_t row) const {
+        return host + ((static_cast<size_t>(layer) * Hkv_loc + h) * 2 + 0) * static_cast<size_t>(max_ctx) * d * 2 +
+               static_cast<size_t>(row) * d * 2;
+    }
+    uint8_t* host_v(int layer, int h, int64_t row) const {
+        return host + ((static_cast<size_t>(layer) * Hkv_loc + h) * 2 + 1) * static_cast<size_t>(max_ctx) * d * 2 +
+               static_cast<size_t>(row) * d * 2;
+    }
+    uint8_t* slot_k(int s) const { return d_stage + static_cast<size_t>(s) * slot_bytes; }
+    uint8_t* slot_v(int s) const { return slot_k(s) + static_cast<size_t>(slot_tokens) * d * 2; }
+};
+
+namespace {
+
+hi_status fail_cuda(hi_ctx* c, cudaError_t e, const char* what) {
+    c->sticky = true;
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+    c->err = buf;
+    return HI_ECUDA;
+}
+
+#define HI_CK(ctx, call)                                     \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return fail_cuda(ctx, e_, #call); \
+    } while (0)
+
+hi_status set_err(hi_ctx* c, hi_status s, const char* msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+int gpu_numa_node(int device) {
+    char bus[64] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return -1;
+    for (char* p = bus; *p; ++p) *p = static_cast<char>(tolower(*p));
+    char path[256];
+    snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bus);
+    FILE* f = fopen(path, "r");
+    if (!f) return -1;
+    int node = -1;
+    if (fscanf(f, "%d", &node) != 1) node = -1;
+    fclose(f);
+    return node;
+}
+
+int numa_node_count() {
+    int n = 0;
+    for (int i = 0; i < 1024; ++i) {
+        char path[128];
+        snprintf(path, sizeof path, "/sys/devices/system/node/node%d", i);
+        if (access(path, F_OK) == 0) ++n;
+        else if (i > 64) break;
+    }
+    return n;
+}
+
+// (a) host KV store: mmap + THP + mbind + parallel first touch + cudaHostRegister
+hi_status alloc_host_store(hi_ctx* c, int numa_policy, int numa_node_req) {
+    const size_t huge = 2u << 20;
+    c->host_map_bytes = (c->host_bytes + huge - 1) / huge * huge;
+    void* p = mmap(nullptr, c->host_map_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (p == MAP_FAILED) return set_err(c, HI_ENOMEM_HOST, "mmap of the host KV store failed");
+    c->host = static_cast<uint8_t*>(p);
+    if (!(c->flags & HI_FLAG_NO_HUGEPAGE)) madvise(p, c->host_map_bytes, MADV_HUGEPAGE);
+    int node = -1;
+    if (numa_policy == 0) node = gpu_numa_node(c->device);
+    else if (numa_policy == 2) node = numa_node_req;
+    if (node >= 0 && numa_node_count() > 1 && node < 1024) {
+        unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+        mask[node / (8 * sizeof(unsigned long))] |= 1ul << (node % (8 * sizeof(unsigned long)));
+        if (syscall(SYS_mbind, p, c->host_map_bytes, MPOL_BIND, mask, 1024, 0) == 0) c->numa_node = node;
+    } else if (node >= 0) {
+        c->numa_node = node;  // single node: already local
+    }
+    // parallel first touch (faults pages in on the bound node before pinning)
+    unsigned nthr = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t per = (c->host_map_bytes / nthr + huge - 1) / huge * huge;
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < nthr; ++i) {
+        const size_t b = i * per;
+        if (b >= c->host_map_bytes) break;
+        const size_t e = std::min(c->host_map_bytes, b + per);
+        th.emplace_back([=] {
+            for (size_t o = b; o < e; o += 4096) c->host[o] = 0;
+        });
+    }
+    for (auto& t : th) t.join();
+    cudaError_t e = cudaHostRegister(p, c->host_map_bytes, cudaHostRegisterDefault);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        char buf[256];
+        snprintf(buf, sizeof buf, "cudaHostRegister of %zu bytes failed: %s", c->host_map_bytes, cudaGetErrorString(e));
+        return set_err(c, e == cudaErrorMemoryAllocation ? HI_ENOMEM_HOST : HI_ECUDA, buf);
+    }
+    c->host_registered = true;
+    return HI_OK;
+}
+
+void destroy(hi_ctx* c) {
+    if (!c) return;
+    if (c->s_comp) cudaStreamSynchronize(c->s_comp);
+    if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
+    if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
+    for (auto& s : c->slots) {
+        if (s.ready) cudaEventDestroy(s.ready);
+        if (s.free_) cudaEventDestroy(s.free_);
+    }
+    for (auto e : c->ev_layer_d2h) if (e) cudaEventDestroy(e);
+    for (auto e : c->ev_kvnew_free) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {c->ev_call_in, c->ev_call_out, c->ev_packed, c->ev_pack_free})
+        if (e) cudaEventDestroy(e);
+    for (cudaStream_t s : {c->s_comp, c->s_h2d, c->s_d2h})
+        if (s) cudaStreamDestroy(s);
+    cudaFree(c->d_stage);
+    cudaFree(c->d_pack);
+    cudaFree(c->d_oacc);
+    cudaFree(c->d_macc);
+    cudaFree(c->d_lacc);
+    cudaFree(c->d_parts);
+    cudaFree(c->d_kvnew);
+    if (c->host) {
+        if (c->host_registered) cudaHostUnregister(c->host);
+        munmap(c->host, c->host_map_bytes);
+    }
+    cudaGetLastError();
+    delete c;
+}
+
+// Split length for the decode partial kernel: ~2 CTAs per SM per history block.
+int decode_split_len(int64_t nk) {
+    int64_t s = (nk + 295) / 296;
+    s = (s + 63) / 64 * 64;
+    return static_cast<int>(std::max<int64_t>(64, std::min<int64_t>(s, 1 << 20)));
+}
+int64_t decode_parts_for_block(int64_t nk) {
+    const int sl = decode_split_len(nk);
+    return (nk + sl - 1) / sl;
+}
+
+hi_status check_call(hi_ctx* c, int layer) {
+    if (!c) return HI_ESHAPE;
+    if (c->sticky) return HI_ECUDA;
+    if (layer < 0 || layer >= c->L) return set_err(c, HI_ESHAPE, "layer out of range");
+    return HI_OK;
+}
+
+// Enqueue the H2D of history block [k0, k0+nk) of (layer, h) into the next slot; the compute
+// stream is made to wait for it.  Returns the slot index through *slot_out.
+hi_status stage_block(hi_ctx* c, int layer, int h, int64_t k0, int64_t nk, int* slot_out) {
+    const int s = c->next_slot;
+    c->next_slot = (c->next_slot + 1) % c->n_slots;
+    Slot& sl = c->slots[s];
+    HI_CK(c, cudaStreamWaitEvent(c->s_h2d, sl.free_, 0));  // WAR: previous consumer of this slot done
+    if (c->flags & HI_FLAG_POISON_SLOTS) {
+        HI_CK(c, hi::launch_poison(c->slot_k(s), c->slot_bytes, c->s_h2d));
+        ++c->launches;
+    }
+    const size_t bytes = static_cast<size_t>(nk) * c->d * 2;
+    HI_CK(c, cudaMemcpyAsync(c->slot_k(s), c->host_k(layer, h, k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
+    HI_CK(c, cudaMemcpyAsync(c->slot_v(s), c->host_v(layer, h, k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
+    HI_CK(c, cudaEventRecord(sl.ready, c->s_h2d));
+    HI_CK(c, cudaStreamWaitEvent(c->s_comp, sl.ready, 0));  // RAW: block landed
+    c->h2d_bytes += static_cast<int64_t>(2 * bytes);
+    *slot_out = s;
+    return HI_OK;
+}
+
+hi_status release_slot(hi_ctx* c, int s) {
+    HI_CK(c, cudaEventRecord(c->slots[s].free_, c->s_comp));
+    return HI_OK;
+}
+
+hi_status finish_call(hi_ctx* c, cudaStream_t cs) {
+    HI_CK(c, cudaEventRecord(c->ev_call_out, c->s_comp));
+    HI_CK(c, cudaStreamWaitEvent(cs, c->ev_call_out, 0));
+    if (c->flags & HI_FLAG_SERIALIZE) HI_CK(c, cudaDeviceSynchronize());
+    return HI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hi_status_str(hi_status s) {
+    switch (s) {
+        case HI_OK: return "HI_OK";
+        case HI_EINVAL: return "HI_EINVAL";
+        case HI_ESHAPE: return "HI_ESHAPE";
+        case HI_ECAPACITY: return "HI_ECAPACITY";
+        case HI_ENOMEM_HOST: return "HI_ENOMEM_HOST";
+        case HI_ENOMEM_DEV: return "HI_ENOMEM_DEV";
+        case HI_ECUDA: return "HI_ECUDA";
+        case HI_ESTATE: return "HI_ESTATE";
+    }
+    return "HI_UNKNOWN";
+}
+
+const char* hi_last_error(const hi_ctx* c) { return c ? c->err.c_str() : g_init_error.c_str(); }
+
+hi_status hi_init(int layers, int q_heads, int kv_heads, int head_dim, int64_t max_ctx, int chunk, int rank,
+                  int world, hi_ctx** out) {
+    return hi_init_ex(layers, q_heads, kv_heads, head_dim, max_ctx, chunk, rank, world, nullptr, out);
+}
+
+hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_t max_ctx, int chunk, int rank,
+                     int world, const hi_options* opt, hi_ctx** out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!out) { g_init_error = "out is NULL"; return HI_EINVAL; }
+    *out = nullptr;
+    if (layers <= 0 || layers > 128 || q_heads <= 0 || kv_heads <= 0 || max_ctx <= 0 || chunk <= 0 || world <= 0 ||
+        rank < 0 || rank >= world || q_heads % kv_heads != 0 || kv_heads % world != 0 ||
+        (head_dim != 64 && head_dim != 128) || max_ctx > (int64_t(1) << 31) || chunk > (1 << 20)) {
+        g_init_error = "invalid configuration (sizes, q_heads % kv_heads, kv_heads % world, head_dim in {64,128})";
+        return HI_EINVAL;
+    }
+    const int g = q_heads / kv_heads;
+    if (g != 1 && g != 2 && g != 4 && g != 8) {
+        g_init_error = "q_heads/kv_heads must be 1, 2, 4 or 8";
+        return HI_EINVAL;
+    }
+    hi_options o{};
+    if (opt) o = *opt;
+    if (o.n_slots == 0) o.n_slots = 4;
+    if (o.n_slots < 2 || o.n_slots > 64 || o.slot_tokens < 0) {
+        g_init_error = "invalid hi_options (n_slots in [2,64], slot_tokens >= 0)";
+        return HI_EINVAL;
+    }
+
+    hi_ctx* c = new hi_ctx();
+    c->L = layers; c->Hq = q_heads; c->Hkv = kv_heads; c->d = head_dim; c->chunk = chunk;
+    c->rank = rank; c->world = world; c->Hq_loc = q_heads / world; c->Hkv_loc = kv_heads / world; c->g = g;
+    c->max_ctx = max_ctx; c->flags = o.flags;
+    c->scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(head_dim)));
+    c->seq_len.assign(layers, 0);
+    c->n_slots = o.n_slots;
+    int64_t st = o.slot_tokens;
+    if (st == 0) st = std::max<int64_t>(64, (max_ctx / o.n_slots) / 64 * 64);
+    c->slot_tokens = st;
+    c->slot_bytes = static_cast<size_t>(st) * head_dim * 2 * 2;
+
+    auto bail = [&](hi_status s, const std::string& msg) {
+        g_init_error = msg.empty() ? c->err : msg;
+        destroy(c);
+        return s;
+    };
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return bail(HI_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    }
+    if (opt && opt->device >= 0 && opt->device < ndev && opt->device != 0) c->device = opt->device;
+    else if (cudaGetDevice(&c->device) != cudaSuccess) c->device = 0;
+    if ((e = cudaSetDevice(c->device)) != cudaSuccess) return bail(HI_ECUDA, cudaGetErrorString(e));
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess && prop.major < 10)
+        return bail(HI_ECUDA, "libheadinfer is built for sm_100a (B200); device compute capability < 10");
+
+    // (a) host store
+    c->host_bytes = static_cast<size_t>(layers) * c->Hkv_loc * 2 * static_cast<size_t>(max_ctx) * head_dim * 2;
+    hi_status hs = alloc_host_store(c, o.numa_policy, o.numa_node);
+    if (hs != HI_OK) return bail(hs, "");
+
+    // (b)/(c) staging, streams, events
+    auto dmalloc = [&](void** p, size_t bytes) -> bool {
+        if (cudaMalloc(p, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
+        return true;
+    };
+    if (!dmalloc(reinterpret_cast<void**>(&c->d_stage), c->slot_bytes * c->n_slots))
+        return bail(HI_ENOMEM_DEV, "cudaMalloc of the staging slots failed");
+    const size_t rows = static_cast<size_t>(chunk) * g;
+    const int64_t max_blocks = (max_ctx + st - 1) / st;
+    c->max_parts = static_cast<int>(max_blocks * decode_parts_for_block(std::min<int64_t>(st, max_ctx)) + 8);
+    const size_t pack_b = static_cast<size_t>(c->Hkv_loc) * 2 * chunk * head_dim * 2;
+    const size_t oacc_b = rows * head_dim * 4, ml_b = rows * 4;
+    const size_t parts_b = static_cast<size_t>(c->Hkv_loc) * c->max_parts * g * (head_dim + 4) * 4;
+    const size_t kvnew_b = static_cast<size_t>(layers) * 2 * c->Hkv_loc * head_dim * 2;
+    if (!dmalloc(reinterpret_cast<void**>(&c->d_pack), pack_b) || !dmalloc(reinterpret_cast<void**>(&c->d_oacc), oacc_b) ||
+        !dmalloc(reinterpret_cast<void**>(&c->d_macc), ml_b) || !dmalloc(reinterpret_cast<void**>(&c->d_lacc), ml_b) ||
+        !dmalloc(reinterpret_cast<void**>(&c->d_parts), parts_b) || !dmalloc(reinterpret_cast<void**>(&c->d_kvnew), kvnew_b))
+        return bail(HI_ENOMEM_DEV, "cudaMalloc of a workspace failed");
+    c->workspace_bytes = static_cast<int64_t>(pack_b + oacc_b + 2 * ml_b + parts_b + kvnew_b);
+
+    auto mkev = [&](cudaEvent_t* ev) { return cudaEventCreateWithFlags(ev, cudaEventDisableTiming) == cudaSuccess; };
+    bool ok = cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking) == cudaSuccess && mkev(&c->ev_call_in) &&
+              mkev(&c->ev_call_out) && mkev(&c->ev_packed) && mkev(&c->ev_pack_free);
+    c->slots.resize(c->n_slots);
+    for (auto& s : c->slots) ok = ok && mkev(&s.ready) && mkev(&s.free_);
+    c->ev_layer_d2h.assign(layers, nullptr);
+    c->ev_kvnew_free.assign(layers, nullptr);
+    for (int l = 0; l < layers; ++l) ok = ok && mkev(&c->ev_layer_d2h[l]) && mkev(&c->ev_kvnew_free[l]);
+    if (!ok) { cudaGetLastError(); return bail(HI_ECUDA, "stream/event creation failed"); }
+    // record every event once so the first waits are satisfied
+    for (auto& s : c->slots) ok = ok && cudaEventRecord(s.free_, c->s_comp) == cudaSuccess;
+    for (int l = 0; l < layers; ++l)
+        ok = ok && cudaEventRecord(c->ev_layer_d2h[l], c->s_d2h) == cudaSuccess &&
+             cudaEventRecord(c->ev_kvnew_free[l], c->s_d2h) == cudaSuccess;
+    ok = ok && cudaEventRecord(c->ev_pack_free, c->s_d2h) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess;
+    if (!ok) { cudaGetLastError(); return bail(HI_ECUDA, "initial event record failed"); }
+    c->init_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = c;
+    return HI_OK;
+}
+
+hi_status hi_free(hi_ctx* c) {
+    destroy(c);
+    return HI_OK;
+}
+
+hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, const void* V, void* out, int n,
+                           void* cuda_stream) {
+    hi_status st = check_call(c, layer);
+    if (st != HI_OK) return st;
+    if (!Q || !K || !V || !out) return set_err(c, HI_ESHAPE, "NULL tensor pointer");
+    if (n < 1 || n > c->chunk) return set_err(c, HI_ESHAPE, "n_tokens must be in [1, chunk]");
+    const int64_t s = c->seq_len[layer];
+    if (s + n > c->max_ctx) return set_err(c, HI_ECAPACITY, "seq_len + n_tokens exceeds max_ctx");
+    cudaStream_t cs = static_cast<cudaStream_t>(cuda_stream);
+    const int d = c->d, Hkv = c->Hkv_loc, g = c->g;
+
+    HI_CK(c, cudaEventRecord(c->ev_call_in, cs));
+    HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_call_in, 0));
+    // pack the chunk's K/V head-major (the previous call's write-back must have drained)
+    HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_pack_free, 0));
+    HI_CK(c, hi::launch_pack_kv(static_cast<const __nv_bfloat16*>(K), static_cast<const __nv_bfloat16*>(V), c->d_pack, n,
+                                Hkv, d, c->s_comp));
+    ++c->launches;
+    HI_CK(c, cudaEventRecord(c->ev_packed, c->s_comp));
+    // history H2D of this layer must see every earlier write-back of its rows (RAW via host DRAM)
+    HI_CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_layer_d2h[layer], 0));
+    // write-back (Alg. 1 line 11): D2H of the chunk's rows [s, s+n) of every local kv head
+    HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
+    const size_t row_bytes = static_cast<size_t>(d) * 2;
+    for (int h = 0; h < Hkv; ++h) {
+        const __nv_bfloat16* pk = c->d_pack + (static_cast<size_t>(h) * 2 + 0) * n * d;
+        const __nv_bfloat16* pv = c->d_pack + (static_cast<size_t>(h) * 2 + 1) * n * d;
+        HI_CK(c, cudaMemcpyAsync(c->host_k(layer, h, s), pk, n * row_bytes, cudaMemcpyDeviceToHost, c->s_d2h));
+        HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, s), pv, n * row_bytes, cudaMemcpyDeviceToHost, c->s_d2h));
+        c->d2h_bytes += static_cast<int64_t>(2 * n * row_bytes);
+    }
+    HI_CK(c, cudaEventRecord(c->ev_pack_free, c->s_d2h));
+    HI_CK(c, cudaEventRecord(c->ev_layer_d2h[layer], c->s_d2h));
+
+    // attention, one kv head at a time (Alg. 1 line 5 loop)
+    const int64_t nb = (s + c->slot_tokens - 1) / c->slot_tokens;
+    hi::PrefillParams p{};
+    p.q_tok_stride = static_cast<int64_t>(c->Hq_loc) * d;
+    p.o_tok_stride = p.q_tok_stride;
+    p.n_q = n;
+    p.q_pos0 = s;
+    p.g = g;
+    p.scale_log2 = c->scale_log2;
+    p.o_acc = c->d_oacc;
+    p.m_acc = c->d_macc;
+    p.l_acc = c->d_lacc;
+    for (int h = 0; h < Hkv; ++h) {
+        p.q = static_cast<const __nv_bfloat16*>(Q) + static_cast<size_t>(h) * g * d;
+        p.out = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(h) * g * d;
+        // the chunk's own keys first: causal, no transfer needed
+        p.k = c->d_pack + (static_cast<size_t>(h) * 2 + 0) * n * d;
+        p.v = c->d_pack + (static_cast<size_t>(h) * 2 + 1) * n * d;
+        p.kv_row_stride = d;
+        p.n_k = n;
+        p.k_pos0 = s;
+        p.flags = hi::PF_FIRST | hi::PF_CAUSAL | (nb == 0 ? hi::PF_LAST : 0);
+        HI_CK(c, hi::launch_prefill(p, d, c->s_comp));
+        ++c->launches;
+        // history blocks [0, s) through the staging slots (Alg. 1 line 10 prefetch)
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t k0 = b * c->slot_tokens;
+            const int64_t nk = std::min<int64_t>(c->slot_tokens, s - k0);
+            int slot = 0;
+            st = stage_block(c, layer, h, k0, nk, &slot);
+            if (st != HI_OK) return st;
+            p.k = reinterpret_cast<const __nv_bfloat16*>(c->slot_k(slot));
+            p.v = reinterpret_cast<const __nv_bfloat16*>(c->slot_v(slot));
+            p.n_k = static_cast<int>(nk);
+            p.k_pos0 = k0;
+            p.flags = (b == nb - 1) ? hi::PF_LAST : 0;
+            HI_CK(c, hi::launch_prefill(p, d, c->s_comp));
+            ++c->launches;
+            st = release_slot(c, slot);
+            if (st != HI_OK) return st;
+        }
+    }
+    st = finish_call(c, cs);
+    if (st != HI_OK) return st;
+    c->seq_len[layer] = s + n;
+    ++c->prefill_calls;
+    return HI_OK;
+}
+
+hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const void* v, void* out, void* cuda_stream) {
+    hi_status st = check_call(c, layer);
+    if (st != HI_OK) return st;
+    if (!q || !k || !v || !out) return set_err(c, HI_ESHAPE, "NULL tensor pointer");
+    const int64_t s = c->seq_len[layer];
+    if (s + 1 > c->max_ctx) return set_err(c, HI_ECAPACITY, "seq_len + 1 exceeds max_ctx");
+    cudaStream_t cs = static_cast<cudaStream_t>(cuda_stream);
+    const int d = c->d, Hkv = c->Hkv_loc, g = c->g;
+    const size_t row_bytes = static_cast<size_t>(d) * 2;
+
+    HI_CK(c, cudaEventRecord(c->ev_call_in, cs));
+    HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_call_in, 0));
+    // copy the new k, v into this layer's kvnew buffer (its previous write-back must be done)
+    __nv_bfloat16* kn = c->d_kvnew + static_cast<size_t>(layer) * 2 * Hkv * d;
+    __nv_bfloat16* vn = kn + static_cast<size_t>(Hkv) * d;
+    HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_kvnew_free[layer], 0));
+    HI_CK(c, cudaMemcpyAsync(kn, k, Hkv * row_bytes, cudaMemcpyDeviceToDevice, c->s_comp));
+    HI_CK(c, cudaMemcpyAsync(vn, v, Hkv * row_bytes, cudaMemcpyDeviceToDevice, c->s_comp));
+    HI_CK(c, cudaEventRecord(c->ev_packed, c->s_comp));
+    HI_CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_layer_d2h[layer], 0));
+    // append (Alg. 1 line 26 "Async Update CPU KV cache"): host row s of every local kv head
+    HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
+    for (int h = 0; h < Hkv; ++h) {
+        HI_CK(c, cudaMemcpyAsync(c->host_k(layer, h, s), kn + static_cast<size_t>(h) * d, row_bytes,
+                                 cudaMemcpyDeviceToHost, c->s_d2h));
+        HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, s), vn + static_cast<size_t>(h) * d, row_bytes,
+                                 cudaMemcpyDeviceToHost, c->s_d2h));
+        c->d2h_bytes += static_cast<int64_t>(2 * row_bytes);
+    }
+    HI_CK(c, cudaEventRecord(c->ev_kvnew_free[layer], c->s_d2h));
+    HI_CK(c, cudaEventRecord(c->ev_layer_d2h[layer], c->s_d2h));
+
+    // history: per kv head, blocks through the slots -> split-K partial records
+    const int64_t nb = (s + c->slot_tokens - 1) / c->slot_tokens;
+    int n_parts = 0;
+    for (int h = 0; h < Hkv; ++h) {
+        int pofs = 0;
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t k0 = b * c->slot_tokens;
+            const int64_t nk = std::min<int64_t>(c->slot_tokens, s - k0);
+            int slot = 0;
+            st = stage_block(c, layer, h, k0, nk, &slot);
+            if (st != HI_OK) return st;
+            hi::DecodePartialParams p{};
+            p.q = static_cast<const __nv_bfloat16*>(q) + static_cast<size_t>(h) * g * d;
+            p.k = reinterpret_cast<const __nv_bfloat16*>(c->slot_k(slot));
+            p.v = reinterpret_cast<const __nv_bfloat16*>(c->slot_v(slot));
+            p.n_k = static_cast<int>(nk);
+            p.split_len = decode_split_len(nk);
+            p.scale_log2 = c->scale_log2;
+            p.parts = c->d_parts + (static_cast<size_t>(h) * c->max_parts + pofs) * g * (d + 4);
+            const int nsp = static_cast<int>((nk + p.split_len - 1) / p.split_len);
+            HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, c->s_comp));
+            ++c->launches;
+            pofs += nsp;
+            st = release_slot(c, slot);
+            if (st != HI_OK) return st;
+        }
+        n_parts = pofs;
+    }
+    hi::DecodeCombineParams cp{};
+    cp.q = static_cast<const __nv_bfloat16*>(q);
+    cp.k_new = kn;
+    cp.v_new = vn;
+    cp.parts = c->d_parts;
+    cp.max_parts = c->max_parts;
+    cp.n_parts = n_parts;
+    cp.g = g;
+    cp.scale_log2 = c->scale_log2;
+    cp.out = static_cast<__nv_bfloat16*>(out);
+    HI_CK(c, hi::launch_decode_combine(cp, d, c->Hq_loc, c->s_comp));
+    ++c->launches;
+    st = finish_call(c, cs);
+    if (st != HI_OK) return st;
+    c->seq_len[layer] = s + 1;
+    ++c->decode_calls;
+    return HI_OK;
+}
+
+hi_status hi_synchronize(hi_ctx* c) {
+    if (!c) return HI_ESHAPE;
+    if (c->sticky) return HI_ECUDA;
+    HI_CK(c, cudaStreamSynchronize(c->s_comp));
+    HI_CK(c, cudaStreamSynchronize(c->s_h2d));
+    HI_CK(c, cudaStreamSynchronize(c->s_d2h));
+    return HI_OK;
+}
+
+hi_status hi_read_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, void* k_dst, void* v_dst) {
+    hi_status st = check_call(c, layer);
+    if (st != HI_OK) return st;
+    if (h < 0 || h >= c->Hkv_loc || pos < 0 || n < 0 || pos + n > c->max_ctx || (n > 0 && (!k_dst || !v_dst)))
+        return set_err(c, HI_ESHAPE, "bad host KV range");
+    HI_CK(c, cudaStreamSynchronize(c->s_d2h));
+    memcpy(k_dst, c->host_k(layer, h, pos), static_cast<size_t>(n) * c->d * 2);
+    memcpy(v_dst, c->host_v(layer, h, pos), static_cast<size_t>(n) * c->d * 2);
+    return HI_OK;
+}
+
+hi_status hi_write_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, const void* k_src, const void* v_src,
+                           int from_device) {
+    hi_status st = check_call(c, layer);
+    if (st != HI_OK) return st;
+    if (h < 0 || h >= c->Hkv_loc || pos < 0 || n < 0 || pos + n > c->max_ctx || (n > 0 && (!k_src || !v_src)))
+        return set_err(c, HI_ESHAPE, "bad host KV range");
+    st = hi_synchronize(c);
+    if (st != HI_OK) return st;
+    const size_t bytes = static_cast<size_t>(n) * c->d * 2;
+    if (from_device) {
+        HI_CK(c, cudaMemcpyAsync(c->host_k(layer, h, pos), k_src, bytes, cudaMemcpyDeviceToHost, c->s_d2h));
+        HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, pos), v_src, bytes, cudaMemcpyDeviceToHost, c->s_d2h));
+        HI_CK(c, cudaStreamSynchronize(c->s_d2h));
+    } else {
+        memcpy(c->host_k(layer, h, pos), k_src, bytes);
+        memcpy(c->host_v(layer, h, pos), v_src, bytes);
+    }
+    return HI_OK;
+}
+
+int64_t hi_seq_len(const hi_ctx* c, int layer) {
+    if (!c || layer < 0 || layer >= c->L) return -1;
+    return c->seq_len[layer];
+}
+
+hi_status hi_set_seq_len(hi_ctx* c, int layer, int64_t s) {
+    hi_status st = check_call(c, layer);
+    if (st != HI_OK) return st;
+    if (s < 0 || s > c->max_ctx) return set_err(c, HI_ESHAPE, "seq_len out of range");
+    st = hi_synchronize(c);
+    if (st != HI_OK) return st;
+    c->seq_len[layer] = s;
+    return HI_OK;
+}
+
+hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
+    if (!c || !o) return HI_ESHAPE;
+    if (!c->sticky) {
+        hi_status st = hi_synchronize(c);
+        if (st != HI_OK) return st;
+    }
+    memset(o, 0, sizeof *o);
+    o->host_store_bytes = static_cast<int64_t>(c->host_bytes);
+    o->staging_bytes = static_cast<int64_t>(c->slot_bytes) * c->n_slots;
+    o->staging_bound_bytes = 4ll * c->d * c->max_ctx;
+    o->workspace_bytes = static_cast<int64_t>(c->workspace_bytes);
+    o->h2d_bytes = c->h2d_bytes;
+    o->d2h_bytes = c->d2h_bytes;
+    o->prefill_calls = c->prefill_calls;
+    o->decode_calls = c->decode_calls;
+    o->kernel_launches = c->launches;
+    o->init_seconds = c->init_seconds;
+    o->numa_node = c->numa_node;
+    o->n_slots = c->n_slots;
+    o->slot_tokens = c->slot_tokens;
+    return HI_OK;
+}
+
+}  // extern "C"

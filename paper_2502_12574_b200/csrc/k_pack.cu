@@ -1,0 +1,56 @@
+// k_pack.cu -- gather the chunk's K and V [n][Hkv][d] into head-major [Hkv][2][n][d]
+// (SURVEY.md §2B K5b), so each head's write-back to host (Alg. 1 line 11) is one
+// contiguous D2H per tensor and the chunk's own keys are a contiguous segment for the
+// prefill kernel.  Pure data movement: 16-byte vector loads/stores, fully coalesced.
+#include "hi_kernels.cuh"
+
+namespace hi {
+namespace {
+
+__global__ void pack_kv_kernel(const uint4* __restrict__ k, const uint4* __restrict__ v, uint4* __restrict__ packed,
+                               int n, int hkv, int cpr /* 16-byte chunks per row */) {
+    const int64_t total = static_cast<int64_t>(n) * hkv * cpr;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % cpr);
+        const int64_t th = i / cpr;  // token*hkv + head
+        const int h = static_cast<int>(th % hkv);
+        const int64_t t = th / hkv;
+        const int64_t dk = ((static_cast<int64_t>(h) * 2 + 0) * n + t) * cpr + c;
+        const int64_t dv = ((static_cast<int64_t>(h) * 2 + 1) * n + t) * cpr + c;
+        packed[dk] = k[i];
+        packed[dv] = v[i];
+    }
+}
+
+__global__ void poison_kernel(uint4* p, int64_t n16) {
+    const uint4 nan4 = make_uint4(0x7fc07fc0u, 0x7fc07fc0u, 0x7fc07fc0u, 0x7fc07fc0u);  // bf16 qNaN pairs
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = nan4;
+}
+
+}  // namespace
+
+cudaError_t launch_pack_kv(const __nv_bfloat16* k, const __nv_bfloat16* v, __nv_bfloat16* packed, int n, int hkv,
+                           int d, cudaStream_t stream) {
+    const int cpr = d / 8;
+    const int64_t total = static_cast<int64_t>(n) * hkv * cpr;
+    if (total == 0) return cudaSuccess;
+    const int threads = 256;
+    const int64_t want = (total + threads - 1) / threads;
+    const int grid = static_cast<int>(want < 148 * 8 ? want : 148 * 8);
+    pack_kv_kernel<<<grid, threads, 0, stream>>>(reinterpret_cast<const uint4*>(k), reinterpret_cast<const uint4*>(v),
+                                                 reinterpret_cast<uint4*>(packed), n, hkv, cpr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_poison(void* ptr, size_t bytes, cudaStream_t stream) {
+    const int64_t n16 = static_cast<int64_t>(bytes / 16);
+    if (n16 == 0) return cudaSuccess;
+    const int64_t want = (n16 + 255) / 256;
+    poison_kernel<<<static_cast<int>(want < 148 * 8 ? want : 148 * 8), 256, 0, stream>>>(reinterpret_cast<uint4*>(ptr), n16);
+    return cudaGetLastError();
+}
+
+}  // namespace hi

@@ -1,0 +1,76 @@
+"""C-ABI contract checks that need no GPU: the library loads, exports every symbol
+include/headinfer.h declares, and fails loudly (HI_ECUDA, no CPU fallback) without a device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import cuda_available
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "headinfer.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hi_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2502_12574_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2502_12574_b200 import build
+        build.build()
+    return _lib.load()
+
+
+def test_header_declares_the_north_star_calls():
+    syms = _declared_symbols()
+    for name in ("hi_init", "hi_prefill_chunk", "hi_decode", "hi_free"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2502_12574_b200 import _lib
+    syms = _declared_symbols()
+    assert sorted(_lib.EXPORTS) == syms
+    for name in syms:
+        assert hasattr(lib, name), name
+
+
+def test_status_strings(lib):
+    names = [lib.hi_status_str(i).decode() for i in range(8)]
+    assert names == ["HI_OK", "HI_EINVAL", "HI_ESHAPE", "HI_ECAPACITY", "HI_ENOMEM_HOST", "HI_ENOMEM_DEV",
+                     "HI_ECUDA", "HI_ESTATE"]
+
+
+def test_free_null_and_bad_handles(lib):
+    assert lib.hi_free(None) == 0
+    assert lib.hi_seq_len(None, 0) == -1
+    assert lib.hi_prefill_chunk(None, 0, None, None, None, None, 1, None) == 2  # HI_ESHAPE
+    assert lib.hi_last_error(None)
+
+
+@pytest.mark.parametrize("args", [
+    (0, 4, 2, 64, 1024, 256, 0, 1),     # layers <= 0
+    (1, 5, 2, 64, 1024, 256, 0, 1),     # q_heads % kv_heads
+    (1, 4, 2, 96, 1024, 256, 0, 1),     # head_dim not in {64, 128}
+    (1, 8, 2, 64, 1024, 256, 0, 4),     # kv_heads % world
+    (1, 4, 2, 64, 0, 256, 0, 1),        # max_ctx <= 0
+    (1, 4, 2, 64, 1024, 256, 1, 1),     # rank >= world
+    (1, 64, 2, 64, 1024, 256, 0, 1),    # g = 32 unsupported
+])
+def test_init_rejects_invalid_configuration(lib, args):
+    h = ctypes.c_void_p()
+    assert lib.hi_init(*args, ctypes.byref(h)) == 1  # HI_EINVAL, before touching CUDA
+    assert not h.value
+
+
+@pytest.mark.skipif(cuda_available(), reason="checks the no-GPU behaviour")
+def test_init_without_gpu_fails_loudly(lib):
+    h = ctypes.c_void_p()
+    assert lib.hi_init(1, 4, 2, 64, 1024, 256, 0, 1, ctypes.byref(h)) == 6  # HI_ECUDA, no CPU fallback
+    assert not h.value
+    assert b"CUDA" in lib.hi_last_error(None) or b"device" in lib.hi_last_error(None)

@@ -1,0 +1,75 @@
+"""C-ABI contract on a GPU: error paths are atomic (no state change), capacity is enforced,
+seq_len bookkeeping, stats, hi_set_seq_len rewinds."""
+import pytest
+import torch
+
+from conftest import cuda_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a GPU")]
+
+
+def _ctx(**kw):
+    from paper_2502_12574_b200.headinfer import HeadInfer
+    return HeadInfer(2, 4, 2, 64, 300, 128, **kw)
+
+
+def _qkv(n, hq=4, hkv=2, d=64):
+    mk = lambda h: torch.randn(n, h, d, device="cuda").clamp(-1, 1).to(torch.bfloat16)
+    return mk(hq), mk(hkv), mk(hkv)
+
+
+def test_error_paths_leave_state_unchanged():
+    from paper_2502_12574_b200._lib import HIError
+    ctx = _ctx()
+    Q, K, V = _qkv(128)
+    ctx.prefill_chunk(0, Q, K, V)
+    assert ctx.seq_len(0) == 128 and ctx.seq_len(1) == 0
+    with pytest.raises(HIError) as e:
+        ctx.prefill_chunk(2, Q, K, V)  # layer out of range
+    assert e.value.status == 2
+    Q2, K2, V2 = _qkv(129)
+    with pytest.raises(HIError) as e:
+        ctx.prefill_chunk(0, Q2, K2, V2)  # n > chunk
+    assert e.value.status == 2
+    ctx.prefill_chunk(0, Q, K, V)  # 256
+    with pytest.raises(HIError) as e:
+        ctx.prefill_chunk(0, Q, K, V)  # 384 > max_ctx 300
+    assert e.value.status == 3
+    assert ctx.seq_len(0) == 256
+    Q3, K3, V3 = _qkv(44)
+    ctx.prefill_chunk(0, Q3, K3, V3)  # exactly max_ctx
+    assert ctx.seq_len(0) == 300
+    q, k, v = _qkv(1)
+    with pytest.raises(HIError) as e:
+        ctx.decode(0, q[0], k[0], v[0])
+    assert e.value.status == 3
+    ctx.decode(1, q[0], k[0], v[0])
+    assert ctx.seq_len(1) == 1
+    st = ctx.stats()
+    assert st["prefill_calls"] == 3 and st["decode_calls"] == 1
+    assert st["d2h_bytes"] == (300 + 1) * 2 * 2 * 64 * 2
+    ctx.set_seq_len(0, 128)
+    assert ctx.seq_len(0) == 128
+    ctx.close()
+
+
+def test_bad_tensor_metadata_rejected_by_binding():
+    ctx = _ctx()
+    Q, K, V = _qkv(16)
+    with pytest.raises(ValueError):
+        ctx.prefill_chunk(0, Q.float(), K, V)
+    with pytest.raises(ValueError):
+        ctx.prefill_chunk(0, Q.cpu(), K, V)
+    with pytest.raises(ValueError):
+        ctx.prefill_chunk(0, Q, K[:, :1], V)
+    assert ctx.seq_len(0) == 0
+    ctx.close()
+
+
+def test_init_reports_host_store_and_residency():
+    ctx = _ctx(n_slots=3)
+    st = ctx.stats()
+    assert st["host_store_bytes"] == 2 * 2 * 2 * 300 * 64 * 2
+    assert st["n_slots"] == 3 and st["slot_tokens"] == 64
+    assert st["staging_bytes"] == 3 * 64 * 4 * 64
+    ctx.close()
