@@ -67,6 +67,9 @@ typedef struct hi_options {
 #define HI_FLAG_POISON_SLOTS 0x1 /* fill each staging slot with NaN before every H2D (race detection) */
 #define HI_FLAG_NO_HUGEPAGE 0x2  /* do not madvise(MADV_HUGEPAGE) the host store */
 #define HI_FLAG_SERIALIZE 0x4    /* synchronise after every internal step (debug; destroys overlap) */
+#define HI_FLAG_TIMING 0x8       /* bracket every attention kernel launch with timing events on the
+                                    compute stream; durations are summed into hi_stats at the next
+                                    hi_synchronize / hi_get_stats (bench roofline evidence) */
 
 typedef struct hi_stats {
     int64_t host_store_bytes;     /* pinned host KV bytes (L * Hkv_loc * max_ctx * 4 * d) */
@@ -77,6 +80,13 @@ typedef struct hi_stats {
     int64_t d2h_bytes;            /* cumulative new-K/V bytes written back device->host */
     int64_t prefill_calls, decode_calls;
     int64_t kernel_launches;      /* cumulative launches of this library's kernels */
+    /* HI_FLAG_TIMING only: attention kernels, device time from CUDA events on the compute stream */
+    double prefill_attn_ms;       /* summed duration of prefill attention launches */
+    double prefill_attn_flops;    /* their algorithmic FLOPs: 4*d*g*(visible (query,key) pairs) */
+    int64_t prefill_attn_launches;
+    double decode_attn_ms;        /* summed duration of decode split-K partial launches */
+    double decode_attn_bytes;     /* their algorithmic HBM bytes: 4*d per key read */
+    int64_t decode_attn_launches;
     double init_seconds;          /* wall time of hi_init (host pinning dominates) */
     int numa_node;                /* node the host store is bound to (-1: none / unknown) */
     int n_slots;

@@ -16,6 +16,7 @@ STATUS_NAMES = ["HI_OK", "HI_EINVAL", "HI_ESHAPE", "HI_ECAPACITY", "HI_ENOMEM_HO
 HI_FLAG_POISON_SLOTS = 0x1
 HI_FLAG_NO_HUGEPAGE = 0x2
 HI_FLAG_SERIALIZE = 0x4
+HI_FLAG_TIMING = 0x8
 
 # every symbol include/headinfer.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",
@@ -33,7 +34,11 @@ class hi_stats(ctypes.Structure):
                 ("staging_bound_bytes", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("prefill_calls", ctypes.c_int64), ("decode_calls", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64), ("init_seconds", ctypes.c_double),
+                ("kernel_launches", ctypes.c_int64),
+                ("prefill_attn_ms", ctypes.c_double), ("prefill_attn_flops", ctypes.c_double),
+                ("prefill_attn_launches", ctypes.c_int64), ("decode_attn_ms", ctypes.c_double),
+                ("decode_attn_bytes", ctypes.c_double), ("decode_attn_launches", ctypes.c_int64),
+                ("init_seconds", ctypes.c_double),
                 ("numa_node", ctypes.c_int), ("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64)]
 
     def as_dict(self) -> dict:

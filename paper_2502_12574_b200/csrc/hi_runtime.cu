@@ -40,6 +40,12 @@ namespace {
 
 thread_local std::string g_init_error = "no error";
 
+struct TimedLaunch {
+    cudaEvent_t start, stop;
+    double work;   // algorithmic FLOPs (prefill) or bytes (decode)
+    bool prefill;
+};
+
 struct Slot {
     cudaEvent_t ready = nullptr;  // recorded on the H2D stream after the block landed
     cudaEvent_t free_ = nullptr;  // recorded on the compute stream after its consumer kernel
@@ -87,6 +93,11 @@ struct hi_ctx {
     // (f) stats
     int64_t h2d_bytes = 0, d2h_bytes = 0, prefill_calls = 0, decode_calls = 0, launches = 0;
     double init_seconds = 0.0;
+    // HI_FLAG_TIMING
+    std::vector<TimedLaunch> timed;
+    std::vector<cudaEvent_t> ev_pool;
+    double prefill_ms = 0, prefill_flops = 0, decode_ms = 0, decode_bytes = 0;
+    int64_t prefill_timed = 0, decode_timed = 0;
 
     uint8_t* host_k(int layer, int h, int64_t row) const {
         return host + ((static_cast<size_t>(layer) * Hkv_loc + h) * 2 + 0) * static_cast<size_t>(max_ctx) * d * 2 +
@@ -197,6 +208,8 @@ void destroy(hi_ctx* c) {
         if (s.ready) cudaEventDestroy(s.ready);
         if (s.free_) cudaEventDestroy(s.free_);
     }
+    for (auto& t : c->timed) { cudaEventDestroy(t.start); cudaEventDestroy(t.stop); }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (auto e : c->ev_layer_d2h) if (e) cudaEventDestroy(e);
     for (auto e : c->ev_kvnew_free) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {c->ev_call_in, c->ev_call_out, c->ev_packed, c->ev_pack_free})
@@ -260,6 +273,50 @@ hi_status stage_block(hi_ctx* c, int layer, int h, int64_t k0, int64_t nk, int* 
 hi_status release_slot(hi_ctx* c, int s) {
     HI_CK(c, cudaEventRecord(c->slots[s].free_, c->s_comp));
     return HI_OK;
+}
+
+cudaEvent_t pool_event(hi_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+}
+
+// Bracket a kernel launch with timing events when HI_FLAG_TIMING is set.
+struct LaunchTimer {
+    hi_ctx* c;
+    cudaEvent_t start = nullptr;
+    LaunchTimer(hi_ctx* ctx) : c(ctx) {
+        if (c->flags & HI_FLAG_TIMING) {
+            start = pool_event(c);
+            if (start) cudaEventRecord(start, c->s_comp);
+        }
+    }
+    void done(double work, bool prefill) {
+        if (!start) return;
+        cudaEvent_t stop = pool_event(c);
+        if (!stop) return;
+        cudaEventRecord(stop, c->s_comp);
+        c->timed.push_back({start, stop, work, prefill});
+    }
+};
+
+void resolve_timing(hi_ctx* c) {
+    for (auto& t : c->timed) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, t.start, t.stop) == cudaSuccess) {
+            if (t.prefill) { c->prefill_ms += ms; c->prefill_flops += t.work; ++c->prefill_timed; }
+            else { c->decode_ms += ms; c->decode_bytes += t.work; ++c->decode_timed; }
+        }
+        c->ev_pool.push_back(t.start);
+        c->ev_pool.push_back(t.stop);
+    }
+    c->timed.clear();
+    cudaGetLastError();
 }
 
 hi_status finish_call(hi_ctx* c, cudaStream_t cs) {
@@ -457,7 +514,11 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
         p.n_k = n;
         p.k_pos0 = s;
         p.flags = hi::PF_FIRST | hi::PF_CAUSAL | (nb == 0 ? hi::PF_LAST : 0);
-        HI_CK(c, hi::launch_prefill(p, d, c->s_comp));
+        {
+            LaunchTimer tm(c);
+            HI_CK(c, hi::launch_prefill(p, d, c->s_comp));
+            tm.done(4.0 * d * g * (static_cast<double>(n) * (n + 1) / 2.0), true);
+        }
         ++c->launches;
         // history blocks [0, s) through the staging slots (Alg. 1 line 10 prefetch)
         for (int64_t b = 0; b < nb; ++b) {
@@ -471,7 +532,11 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
             p.n_k = static_cast<int>(nk);
             p.k_pos0 = k0;
             p.flags = (b == nb - 1) ? hi::PF_LAST : 0;
-            HI_CK(c, hi::launch_prefill(p, d, c->s_comp));
+            {
+                LaunchTimer tm(c);
+                HI_CK(c, hi::launch_prefill(p, d, c->s_comp));
+                tm.done(4.0 * d * g * static_cast<double>(n) * static_cast<double>(nk), true);
+            }
             ++c->launches;
             st = release_slot(c, slot);
             if (st != HI_OK) return st;
@@ -536,7 +601,11 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
             p.scale_log2 = c->scale_log2;
             p.parts = c->d_parts + (static_cast<size_t>(h) * c->max_parts + pofs) * g * (d + 4);
             const int nsp = static_cast<int>((nk + p.split_len - 1) / p.split_len);
-            HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, c->s_comp));
+            {
+                LaunchTimer tm(c);
+                HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, c->s_comp));
+                tm.done(4.0 * d * static_cast<double>(nk), false);
+            }
             ++c->launches;
             pofs += nsp;
             st = release_slot(c, slot);
@@ -569,6 +638,7 @@ hi_status hi_synchronize(hi_ctx* c) {
     HI_CK(c, cudaStreamSynchronize(c->s_comp));
     HI_CK(c, cudaStreamSynchronize(c->s_h2d));
     HI_CK(c, cudaStreamSynchronize(c->s_d2h));
+    resolve_timing(c);
     return HI_OK;
 }
 
@@ -634,6 +704,12 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     o->prefill_calls = c->prefill_calls;
     o->decode_calls = c->decode_calls;
     o->kernel_launches = c->launches;
+    o->prefill_attn_ms = c->prefill_ms;
+    o->prefill_attn_flops = c->prefill_flops;
+    o->prefill_attn_launches = c->prefill_timed;
+    o->decode_attn_ms = c->decode_ms;
+    o->decode_attn_bytes = c->decode_bytes;
+    o->decode_attn_launches = c->decode_timed;
     o->init_seconds = c->init_seconds;
     o->numa_node = c->numa_node;
     o->n_slots = c->n_slots;
