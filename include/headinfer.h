@@ -70,6 +70,8 @@ typedef struct hi_options {
 #define HI_FLAG_TIMING 0x8       /* bracket every attention kernel launch with timing events on the
                                     compute stream; durations are summed into hi_stats at the next
                                     hi_synchronize / hi_get_stats (bench roofline evidence) */
+#define HI_FLAG_MMA_SYNC_PREFILL 0x10 /* run prefill attention on the legacy mma.sync kernel instead of the
+                                         tcgen05/TMEM/TMA kernel (baseline comparator for benches only) */
 
 typedef struct hi_stats {
     int64_t host_store_bytes;     /* pinned host KV bytes (L * Hkv_loc * max_ctx * 4 * d) */

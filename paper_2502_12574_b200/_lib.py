@@ -17,6 +17,7 @@ HI_FLAG_POISON_SLOTS = 0x1
 HI_FLAG_NO_HUGEPAGE = 0x2
 HI_FLAG_SERIALIZE = 0x4
 HI_FLAG_TIMING = 0x8
+HI_FLAG_MMA_SYNC_PREFILL = 0x10
 
 # every symbol include/headinfer.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",

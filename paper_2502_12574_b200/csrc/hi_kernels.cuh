@@ -35,7 +35,10 @@ struct PrefillParams {
     float* l_acc;             // [n_q*g]
     int flags;
 };
-cudaError_t launch_prefill(const PrefillParams& p, int d, cudaStream_t stream);
+// sm_100a kernel: TMA + tcgen05.mma + TMEM (k_prefill_tc.cu) -- the product path
+cudaError_t launch_prefill_tc(const PrefillParams& p, int d, cudaStream_t stream);
+// baseline comparator: mma.sync m16n8k16 (k_prefill_mma.cu), selected by HI_FLAG_MMA_SYNC_PREFILL
+cudaError_t launch_prefill_mma(const PrefillParams& p, int d, cudaStream_t stream);
 
 // ---- decode: split-K partials over one history block + LSE combine (a8) ----------------
 struct DecodePartialParams {

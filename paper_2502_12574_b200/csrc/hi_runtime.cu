@@ -242,6 +242,11 @@ int64_t decode_parts_for_block(int64_t nk) {
     return (nk + sl - 1) / sl;
 }
 
+cudaError_t launch_prefill(hi_ctx* c, const hi::PrefillParams& p) {
+    return (c->flags & HI_FLAG_MMA_SYNC_PREFILL) ? hi::launch_prefill_mma(p, c->d, c->s_comp)
+                                                 : hi::launch_prefill_tc(p, c->d, c->s_comp);
+}
+
 hi_status check_call(hi_ctx* c, int layer) {
     if (!c) return HI_ESHAPE;
     if (c->sticky) return HI_ECUDA;
@@ -516,7 +521,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
         p.flags = hi::PF_FIRST | hi::PF_CAUSAL | (nb == 0 ? hi::PF_LAST : 0);
         {
             LaunchTimer tm(c);
-            HI_CK(c, hi::launch_prefill(p, d, c->s_comp));
+            HI_CK(c, launch_prefill(c, p));
             tm.done(4.0 * d * g * (static_cast<double>(n) * (n + 1) / 2.0), true);
         }
         ++c->launches;
@@ -534,7 +539,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
             p.flags = (b == nb - 1) ? hi::PF_LAST : 0;
             {
                 LaunchTimer tm(c);
-                HI_CK(c, hi::launch_prefill(p, d, c->s_comp));
+                HI_CK(c, launch_prefill(c, p));
                 tm.done(4.0 * d * g * static_cast<double>(n) * static_cast<double>(nk), true);
             }
             ++c->launches;

@@ -6,7 +6,7 @@
 // contiguous key segment into the running state (O, m, l) kept in HBM, so history blocks can
 // be consumed in the order the copy engine lands them (Alg. 1 line 10/13).
 //
-// This is the first (baseline) tensor-core path: warp-level mma.sync m16n8k16 bf16 with
+// BASELINE COMPARATOR (HI_FLAG_MMA_SYNC_PREFILL): the pre-Blackwell tensor-core path: warp-level mma.sync m16n8k16 bf16 with
 // fp32 accumulation, cp.async double-buffered K/V tiles, XOR-swizzled shared memory and
 // ldmatrix operand loads.  Tile: 128 query rows (GQA-packed: rows r = t*g + j) x 64 keys,
 // 8 warps x 16 rows.
@@ -303,7 +303,7 @@ cudaError_t launch_d(const PrefillParams& p, cudaStream_t stream) {
 
 }  // namespace
 
-cudaError_t launch_prefill(const PrefillParams& p, int d, cudaStream_t stream) {
+cudaError_t launch_prefill_mma(const PrefillParams& p, int d, cudaStream_t stream) {
     if (d == 64) return launch_d<64>(p, stream);
     if (d == 128) return launch_d<128>(p, stream);
     return cudaErrorInvalidValue;

@@ -1,0 +1,525 @@
+// k_prefill_tc.cu -- sm_100a prefill attention over one KV segment: TMA -> SMEM -> tcgen05.mma
+// with S and O accumulators in TMEM, fp32 online softmax on CUDA cores, warp-specialised.
+//
+// for q head j of group h and chunk positions p in [s, s+n),
+//   o = sum_{i<=p} softmax_i(q_p . k_i / sqrt(d)) v_i                  (Eq. 9)
+// over history (staging-slot blocks) and the chunk itself (causal, reading R2).  A launch folds
+// ONE contiguous key segment into the running state (O, m, l) held in HBM (same contract as the
+// baseline k_prefill_mma.cu), so history blocks are consumed in the order the copy engine lands
+// them (Alg. 1 line 10/13).  Prefill is a dense contraction (compute-bound for
+// S >= 10K, §5), so both products run on the 5th-gen tensor cores:
+//
+//   S = Q K^T   tcgen05.mma kind::f16, A = Q tile (SMEM, K-major SW128), B = K tile (SMEM,
+//               K-major SW128), D = S in TMEM (fp32, 128 lanes x 128 cols, double-buffered)
+//   O += P V    A = P (bf16, SMEM, K-major SW128, written by the softmax warps),
+//               B = V tile (SMEM, MN-major SW128), D = O in TMEM (fp32, 128 lanes x d cols)
+//
+// CTA = one 128-row Q tile (GQA-packed: row r = t*g + j, loaded by one 3-D TMA box per 64
+// columns), KV tiles of 128 keys.  Warps 0-3: softmax + correction + epilogue (thread i owns TMEM
+// lane / row 32w+i); warp 4: TMA producer; warp 5: TMEM allocator + single-thread MMA issuer.
+// Online softmax in the log2 domain with lazy rescaling (the O correction is applied only when a
+// row max grows by more than 2^8), which is exact: O/l does not depend on the reference max.
+#include "hi_kernels.cuh"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include <mutex>
+
+namespace hi {
+namespace {
+
+constexpr int BM = 128;            // query rows per CTA (TMEM lanes)
+constexpr int BN = 128;            // keys per KV tile
+constexpr int NS = 2;              // K/V pipeline stages
+constexpr int NUM_THREADS = 192;   // 4 softmax warps + TMA warp + MMA warp
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+#define HI_R32(a) "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]), "=r"(a[7]), \
+    "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]), "=r"(a[13]), "=r"(a[14]), "=r"(a[15]),        \
+    "=r"(a[16]), "=r"(a[17]), "=r"(a[18]), "=r"(a[19]), "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]),      \
+    "=r"(a[24]), "=r"(a[25]), "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]), "=r"(a[31])
+#define HI_W32(a) "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), \
+    "r"(a[8]), "r"(a[9]), "r"(a[10]), "r"(a[11]), "r"(a[12]), "r"(a[13]), "r"(a[14]), "r"(a[15]),        \
+    "r"(a[16]), "r"(a[17]), "r"(a[18]), "r"(a[19]), "r"(a[20]), "r"(a[21]), "r"(a[22]), "r"(a[23]),      \
+    "r"(a[24]), "r"(a[25]), "r"(a[26]), "r"(a[27]), "r"(a[28]), "r"(a[29]), "r"(a[30]), "r"(a[31])
+
+// 32 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : HI_R32(r)
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        HI_W32(r)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// UMMA shared-memory descriptor (sm_100 "version 1"), SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // version (sm_100)
+    d |= static_cast<uint64_t>(2) << 61;  // layout: SWIZZLE_128B
+    return d;
+}
+// Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, A K-major, B K- or MN-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
+           (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+struct __align__(8) Barriers {
+    uint64_t q_full;
+    uint64_t k_full[NS], v_full[NS], kv_empty[NS];
+    uint64_t s_full[2], s_free[2];
+    uint64_t p_full, o_done;
+    uint32_t tmem_base;
+};
+
+template <int D>
+struct Smem {
+    static constexpr int BOX = BM * 128;            // one [128 rows][64 bf16] SW128 box = 16 KiB
+    static constexpr int Q_OFF = 0;
+    static constexpr int K_OFF = Q_OFF + (D / 64) * BOX;
+    static constexpr int V_OFF = K_OFF + NS * (D / 64) * BOX;
+    static constexpr int P_OFF = V_OFF + NS * (D / 64) * BOX;
+    static constexpr int BAR_OFF = P_OFF + (BN / 64) * BOX;
+    static constexpr int BYTES = BAR_OFF + 256;
+    static constexpr int ALLOC = BYTES + 1024;      // slack for 1 KiB alignment
+};
+
+template <int D>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_v, const PrefillParams p) {
+    using L = Smem<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Barriers* bars = reinterpret_cast<Barriers*>(smem + L::BAR_OFF);
+    const uint32_t sbase = smem_addr(smem);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = p.g;
+    const int n_rows = p.n_q * g;
+    const int row0 = blockIdx.x * BM;
+    const bool first = p.flags & PF_FIRST, last = p.flags & PF_LAST, causal = p.flags & PF_CAUSAL;
+
+    // keys of the segment visible to this tile (causal: key c visible to token t iff k_pos0+c <= q_pos0+t)
+    const int t_lo = row0 / g;
+    const int t_hi = min(p.n_q - 1, (row0 + BM - 1) / g);
+    int n_k_eff = p.n_k;
+    if (causal) {
+        const int64_t lim = p.q_pos0 + t_hi - p.k_pos0 + 1;
+        const int64_t e = lim < n_k_eff ? lim : static_cast<int64_t>(n_k_eff);
+        n_k_eff = static_cast<int>(e > 0 ? e : 0);
+    }
+    const int n_kt = (n_k_eff + BN - 1) / BN;
+
+    const uint32_t bar_q = smem_addr(&bars->q_full);
+    auto bar_k = [&](int s) { return smem_addr(&bars->k_full[s]); };
+    auto bar_v = [&](int s) { return smem_addr(&bars->v_full[s]); };
+    auto bar_e = [&](int s) { return smem_addr(&bars->kv_empty[s]); };
+    auto bar_sf = [&](int b) { return smem_addr(&bars->s_full[b]); };
+    auto bar_sr = [&](int b) { return smem_addr(&bars->s_free[b]); };
+    const uint32_t bar_p = smem_addr(&bars->p_full);
+    const uint32_t bar_o = smem_addr(&bars->o_done);
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar_q, 1);
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(bar_k(s), 1);
+            mbar_init(bar_v(s), 1);
+            mbar_init(bar_e(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar_sf(b), 1);
+            mbar_init(bar_sr(b), 128);
+        }
+        mbar_init(bar_p, 128);
+        mbar_init(bar_o, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 5) {  // TMEM: S0 [0,128), S1 [128,256), O [256, 256+D)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&bars->tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+    const uint32_t tmem_o = tmem + 256;
+
+    if (warp == 4) {
+        // ============================ TMA producer ============================
+        if (lane == 0 && n_kt > 0) {
+            mbar_expect_tx(bar_q, (D / 64) * L::BOX);
+            for (int c = 0; c < D / 64; ++c)
+                tma_load_3d(sbase + L::Q_OFF + c * L::BOX, &tm_q, bar_q, c * 64, 0, row0 / g);
+            for (int i = 0; i < n_kt; ++i) {
+                const int s = i % NS;
+                if (i >= NS) mbar_wait(bar_e(s), ((i / NS) - 1) & 1);
+                mbar_expect_tx(bar_k(s), (D / 64) * L::BOX);
+                for (int c = 0; c < D / 64; ++c)
+                    tma_load_2d(sbase + L::K_OFF + (s * (D / 64) + c) * L::BOX, &tm_k, bar_k(s), c * 64, i * BN);
+                mbar_expect_tx(bar_v(s), (D / 64) * L::BOX);
+                for (int c = 0; c < D / 64; ++c)
+                    tma_load_2d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, i * BN);
+            }
+        }
+    } else if (warp == 5) {
+        // ============================ MMA issuer ==============================
+        constexpr uint32_t ID_S = idesc_bf16(BM, BN, false);
+        constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
+        if (lane == 0 && n_kt > 0) {
+            mbar_wait(bar_q, 0);
+            auto issue_s = [&](int i) {
+                const int s = i % NS, b = i & 1;
+                mbar_wait(bar_k(s), (i / NS) & 1);
+                if (i >= 2) mbar_wait(bar_sr(b), ((i - 2) >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    const uint32_t off = (ks >> 2) * L::BOX + (ks & 3) * 32;
+                    const uint64_t a = sdesc(sbase + L::Q_OFF + off, 16, 1024);
+                    const uint64_t bdesc = sdesc(sbase + L::K_OFF + s * (D / 64) * L::BOX + off, 16, 1024);
+                    umma_bf16(tmem + b * BN, a, bdesc, ID_S, ks > 0);
+                }
+                umma_commit(bar_sf(b));
+            };
+            issue_s(0);
+            for (int j = 0; j < n_kt; ++j) {
+                if (j + 1 < n_kt) issue_s(j + 1);
+                const int s = j % NS;
+                mbar_wait(bar_p, j & 1);
+                mbar_wait(bar_v(s), (j / NS) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < BN / 16; ++kk) {
+                    const uint64_t a = sdesc(sbase + L::P_OFF + (kk >> 2) * L::BOX + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bdesc = sdesc(sbase + L::V_OFF + s * (D / 64) * L::BOX + kk * 16 * 128, L::BOX, 1024);
+                    umma_bf16(tmem_o, a, bdesc, ID_O, (j > 0 || kk > 0 || !first) ? 1u : 0u);
+                }
+                umma_commit(bar_e(s));
+                umma_commit(bar_o);
+            }
+        }
+    } else {
+        // ====================== softmax / correction / epilogue (warps 0-3) ======================
+        const int r = warp * 32 + lane;           // tile row == TMEM lane
+        const int rg = row0 + r;                  // packed row index t*g + j
+        const bool row_valid = rg < n_rows;
+        const int t = row_valid ? rg / g : 0;
+        const int64_t qpos = p.q_pos0 + t;
+        const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+        const float sc = p.scale_log2;
+        float m_run = -CUDART_INF_F, l_run = 0.f;
+        if (!first) {
+            m_run = row_valid ? p.m_acc[rg] : -CUDART_INF_F;
+            l_run = row_valid ? p.l_acc[rg] : 0.f;
+            if (n_kt > 0) {  // running O -> TMEM before the first PV accumulates onto it
+#pragma unroll
+                for (int cb = 0; cb < D / 32; ++cb) {
+                    uint32_t v[32];
+                    const float4* src = reinterpret_cast<const float4*>(p.o_acc + static_cast<int64_t>(row_valid ? rg : 0) * D + cb * 32);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float4 f = row_valid ? src[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        v[4 * i] = __float_as_uint(f.x); v[4 * i + 1] = __float_as_uint(f.y);
+                        v[4 * i + 2] = __float_as_uint(f.z); v[4 * i + 3] = __float_as_uint(f.w);
+                    }
+                    tmem_st32(tmem_o + lane_addr + cb * 32, v);
+                }
+                tmem_wait_st();
+            }
+        }
+        uint8_t* sP = smem + L::P_OFF;
+        for (int j = 0; j < n_kt; ++j) {
+            const int b = j & 1;
+            mbar_wait(bar_sf(b), (j >> 1) & 1);
+            tc_fence_after();
+            float x[BN];
+#pragma unroll
+            for (int cb = 0; cb < BN / 32; ++cb) {
+                uint32_t v[32];
+                tmem_ld32(tmem + b * BN + lane_addr + cb * 32, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) x[cb * 32 + i] = __uint_as_float(v[i]);
+            }
+            tc_fence_before();
+            mbar_arrive(bar_sr(b));  // S buffer b may be overwritten by S(j+2)
+            // mask: keys beyond the segment / not yet visible (causal)
+            const int key0 = j * BN;
+            const bool need_mask = (key0 + BN > n_k_eff) || (causal && p.k_pos0 + key0 + BN - 1 > p.q_pos0 + t_lo);
+            float mx = -CUDART_INF_F;
+            if (need_mask) {
+                const int64_t lim = qpos - p.k_pos0;  // key index visible iff key <= lim (causal)
+#pragma unroll
+                for (int i = 0; i < BN; ++i) {
+                    const int key = key0 + i;
+                    const bool vis = key < n_k_eff && (!causal || key <= lim);
+                    x[i] = vis ? x[i] * sc : -CUDART_INF_F;
+                    mx = fmaxf(mx, x[i]);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < BN; ++i) {
+                    x[i] *= sc;
+                    mx = fmaxf(mx, x[i]);
+                }
+            }
+            // lazy rescale: move the reference max only when it grows by > 2^8
+            float m_ref = m_run, alpha = 1.f;
+            const bool grow = mx > m_run + RESCALE_THRESHOLD || (m_run == -CUDART_INF_F && mx != -CUDART_INF_F);
+            if (grow) {
+                m_ref = mx;
+                alpha = (m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mx);
+            }
+            const float m_use = (m_ref == -CUDART_INF_F) ? 0.f : m_ref;
+            float lsum = 0.f;
+#pragma unroll
+            for (int i = 0; i < BN; ++i) {
+                x[i] = ex2(x[i] - m_use);
+                lsum += x[i];
+            }
+            // PV(j-1) must be complete before P is overwritten / O is corrected
+            if (j > 0) {
+                mbar_wait(bar_o, (j - 1) & 1);
+                tc_fence_after();
+            }
+            const bool o_live = !first || j > 0;
+            if (o_live && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+                for (int cb = 0; cb < D / 32; ++cb) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem_o + lane_addr + cb * 32, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+                    tmem_st32(tmem_o + lane_addr + cb * 32, v);
+                }
+                tmem_wait_st();
+            }
+            l_run = l_run * alpha + lsum;
+            m_run = m_ref;
+            // P (bf16) -> SMEM, K-major SWIZZLE_128B: row r, 16-byte chunk c of 64-key block kb
+#pragma unroll
+            for (int kb = 0; kb < BN / 64; ++kb) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float* xs = x + kb * 64 + c * 8;
+                    uint4 w;
+                    w.x = pack_bf16(xs[0], xs[1]);
+                    w.y = pack_bf16(xs[2], xs[3]);
+                    w.z = pack_bf16(xs[4], xs[5]);
+                    w.w = pack_bf16(xs[6], xs[7]);
+                    *reinterpret_cast<uint4*>(sP + kb * L::BOX + r * 128 + ((c ^ (r & 7)) << 4)) = w;
+                }
+            }
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(bar_p);
+        }
+        // ---- epilogue ----
+        if (n_kt > 0) {
+            mbar_wait(bar_o, (n_kt - 1) & 1);
+            tc_fence_after();
+        }
+        if (last) {
+            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+            __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (rg % g) * D;
+#pragma unroll
+            for (int cb = 0; cb < D / 32; ++cb) {
+                uint32_t v[32];
+                if (n_kt > 0) {
+                    tmem_ld32(tmem_o + lane_addr + cb * 32, v);
+                    tmem_wait_ld();
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        v[i] = (row_valid && !first) ? __float_as_uint(p.o_acc[static_cast<int64_t>(rg) * D + cb * 32 + i]) : 0u;
+                }
+                if (row_valid) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        uint4 w;
+                        w.x = pack_bf16(__uint_as_float(v[8 * i]) * inv, __uint_as_float(v[8 * i + 1]) * inv);
+                        w.y = pack_bf16(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv);
+                        w.z = pack_bf16(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv);
+                        w.w = pack_bf16(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv);
+                        *reinterpret_cast<uint4*>(dst + cb * 32 + 8 * i) = w;
+                    }
+                }
+            }
+        } else if (n_kt > 0) {
+#pragma unroll
+            for (int cb = 0; cb < D / 32; ++cb) {
+                uint32_t v[32];
+                tmem_ld32(tmem_o + lane_addr + cb * 32, v);
+                tmem_wait_ld();
+                if (row_valid) {
+                    float4* dst = reinterpret_cast<float4*>(p.o_acc + static_cast<int64_t>(rg) * D + cb * 32);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                             __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                }
+            }
+            if (row_valid) {
+                p.m_acc[rg] = m_run;
+                p.l_acc[rg] = l_run;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(ptr);
+    });
+    return fn;
+}
+
+bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
+            const cuuint32_t* box) {
+    EncodeFn fn = get_encode();
+    if (!fn) return false;
+    cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides_bytes, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D>
+cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
+    const int n_rows = p.n_q * p.g;
+    const int grid = (n_rows + BM - 1) / BM;
+    if (grid == 0) return cudaSuccess;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(prefill_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<D>::ALLOC);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    CUtensorMap tq, tk, tv;
+    {
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.g), static_cast<cuuint64_t>(p.n_q)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(p.q_tok_stride) * 2};
+        const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(p.g), static_cast<cuuint32_t>(BM / p.g)};
+        if (!encode(&tq, p.q, 3, dims, strides, box)) return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.kv_row_stride) * 2};
+        const cuuint32_t box[2] = {64, BN};
+        if (!encode(&tk, p.k, 2, dims, strides, box)) return cudaErrorInvalidValue;
+        if (!encode(&tv, p.v, 2, dims, strides, box)) return cudaErrorInvalidValue;
+    }
+    prefill_tc_kernel<D><<<grid, NUM_THREADS, Smem<D>::ALLOC, stream>>>(tq, tk, tv, p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_prefill_tc(const PrefillParams& p, int d, cudaStream_t stream) {
+    if (d == 64) return launch_tc<64>(p, stream);
+    if (d == 128) return launch_tc<128>(p, stream);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace hi
