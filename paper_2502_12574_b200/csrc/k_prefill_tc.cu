@@ -14,9 +14,13 @@
 //   O += P V    A = P (bf16, SMEM, K-major SW128, written by the softmax warps),
 //               B = V tile (SMEM, MN-major SW128), D = O in TMEM (fp32, 128 lanes x d cols)
 //
-// CTA = one 128-row Q tile (GQA-packed: row r = t*g + j, loaded by one 3-D TMA box per 64
-// columns), KV tiles of 128 keys.  Warps 0-3: softmax + correction + epilogue (thread i owns TMEM
-// lane / row 32w+i); warp 4: TMA producer; warp 5: TMEM allocator + single-thread MMA issuer.
+// CTA = two 128-row Q tiles (GQA-packed: row r = t*g + j, loaded by one 3-D TMA box per 64
+// columns) sharing every K/V tile of 128 keys (halves the K/V SMEM/L2 traffic per FLOP).  Warps 0-3
+// own tile 0 and warps 4-7 tile 1 (softmax + O correction + epilogue; thread i owns TMEM lane /
+// row 32*(w%4)+i); warp 8: TMA producer; warp 9: TMEM allocator + single-thread MMA issuer.  P is
+// written back into the S columns of TMEM as packed bf16 and consumed from TMEM by the PV MMA
+// (A operand in TMEM), so P never touches shared memory; the MMA issuer alternates between the two
+// tiles, so one tile's softmax overlaps the other tile's QK^T / PV on the tensor core.
 // Online softmax in the log2 domain with lazy rescaling (the O correction is applied only when a
 // row max grows by more than 2^8), which is exact: O/l does not depend on the reference max.
 #include "hi_kernels.cuh"
@@ -33,7 +37,7 @@ namespace {
 constexpr int BM = 128;            // query rows per CTA (TMEM lanes)
 constexpr int BN = 128;            // keys per KV tile
 constexpr int NS = 2;              // K/V pipeline stages
-constexpr int NUM_THREADS = 192;   // 4 softmax warps + TMA warp + MMA warp
+constexpr int NUM_THREADS = 384;   // 2 x 4 softmax warps (one Q tile each) + TMA warp + MMA warp + 2 spare
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -50,16 +54,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
+// Wait for the phase with the given parity to complete.  A bounded spin (~2^31 polls) turns a
+// pipeline deadlock into a trap (sticky launch error) instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
+    uint32_t done = 0;
+    for (uint32_t it = 0;; ++it) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (it > (1u << 31)) __trap();
+    }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
     asm volatile(
@@ -75,7 +86,6 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -86,6 +96,18 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
         "}\n" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// A operand from TMEM (P), B from shared memory (V)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
@@ -148,23 +170,28 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major)
 struct __align__(8) Barriers {
     uint64_t q_full;
     uint64_t k_full[NS], v_full[NS], kv_empty[NS];
-    uint64_t s_full[2], s_free[2];
-    uint64_t p_full, o_done;
+    uint64_t s_full[2], p_full[2], o_done[2];
     uint32_t tmem_base;
 };
 
 template <int D>
 struct Smem {
     static constexpr int BOX = BM * 128;            // one [128 rows][64 bf16] SW128 box = 16 KiB
-    static constexpr int Q_OFF = 0;
-    static constexpr int K_OFF = Q_OFF + (D / 64) * BOX;
+    static constexpr int Q_OFF = 0;                 // 2 Q tiles x D/64 boxes
+    static constexpr int K_OFF = Q_OFF + 2 * (D / 64) * BOX;
     static constexpr int V_OFF = K_OFF + NS * (D / 64) * BOX;
-    static constexpr int P_OFF = V_OFF + NS * (D / 64) * BOX;
-    static constexpr int BAR_OFF = P_OFF + (BN / 64) * BOX;
+    static constexpr int BAR_OFF = V_OFF + NS * (D / 64) * BOX;
     static constexpr int BYTES = BAR_OFF + 256;
     static constexpr int ALLOC = BYTES + 1024;      // slack for 1 KiB alignment
 };
 
+// Register budget: the launch grants 168 regs x 384 threads; setmaxnreg.inc blocks until the pool
+// can satisfy it, so 2 x 128 x 208 (softmax) + 128 x 88 (TMA/MMA group) must be <= 168 x 384.
+__device__ __forceinline__ void setmaxnreg_inc_208() { asm volatile("setmaxnreg.inc.sync.aligned.u32 208;"); }
+__device__ __forceinline__ void setmaxnreg_dec_88() { asm volatile("setmaxnreg.dec.sync.aligned.u32 88;"); }
+
+// TMEM column map (512 allocated): tile tt in {0,1}: S/P at [256*tt, 256*tt+128), O at [256*tt+128, +D).
+// P (bf16, packed in pairs) overwrites the first 64 columns of S after the row has been read.
 template <int D>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -178,28 +205,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = p.g;
     const int n_rows = p.n_q * g;
-    const int row0 = blockIdx.x * BM;
+    const int row0 = blockIdx.x * (2 * BM);
     const bool first = p.flags & PF_FIRST, last = p.flags & PF_LAST, causal = p.flags & PF_CAUSAL;
+    const int n_tiles = (row0 + BM < n_rows) ? 2 : 1;  // second Q tile may be empty at the tail
 
-    // keys of the segment visible to this tile (causal: key c visible to token t iff k_pos0+c <= q_pos0+t)
-    const int t_lo = row0 / g;
-    const int t_hi = min(p.n_q - 1, (row0 + BM - 1) / g);
-    int n_k_eff = p.n_k;
-    if (causal) {
-        const int64_t lim = p.q_pos0 + t_hi - p.k_pos0 + 1;
-        const int64_t e = lim < n_k_eff ? lim : static_cast<int64_t>(n_k_eff);
-        n_k_eff = static_cast<int>(e > 0 ? e : 0);
-    }
-    const int n_kt = (n_k_eff + BN - 1) / BN;
+    // keys of the segment visible to tile tt (causal: key c visible to token t iff k_pos0+c <= q_pos0+t)
+    auto kt_count = [&](int tt) {
+        const int r0 = row0 + tt * BM;
+        const int t_hi = min(p.n_q - 1, (r0 + BM - 1) / g);
+        int64_t e = p.n_k;
+        if (causal) {
+            const int64_t lim = p.q_pos0 + t_hi - p.k_pos0 + 1;
+            e = lim < e ? lim : e;
+        }
+        e = e > 0 ? e : 0;
+        return static_cast<int>((e + BN - 1) / BN);
+    };
+    const int n_kt0 = kt_count(0);
+    const int n_kt1 = n_tiles == 2 ? kt_count(1) : 0;
+    const int n_kt = max(n_kt0, n_kt1);  // KV tiles streamed through shared memory
 
     const uint32_t bar_q = smem_addr(&bars->q_full);
     auto bar_k = [&](int s) { return smem_addr(&bars->k_full[s]); };
     auto bar_v = [&](int s) { return smem_addr(&bars->v_full[s]); };
     auto bar_e = [&](int s) { return smem_addr(&bars->kv_empty[s]); };
-    auto bar_sf = [&](int b) { return smem_addr(&bars->s_full[b]); };
-    auto bar_sr = [&](int b) { return smem_addr(&bars->s_free[b]); };
-    const uint32_t bar_p = smem_addr(&bars->p_full);
-    const uint32_t bar_o = smem_addr(&bars->o_done);
+    auto bar_s = [&](int t) { return smem_addr(&bars->s_full[t]); };
+    auto bar_p = [&](int t) { return smem_addr(&bars->p_full[t]); };
+    auto bar_o = [&](int t) { return smem_addr(&bars->o_done[t]); };
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
@@ -208,15 +240,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(bar_v(s), 1);
             mbar_init(bar_e(s), 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(bar_sf(b), 1);
-            mbar_init(bar_sr(b), 128);
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(bar_s(t), 1);
+            mbar_init(bar_p(t), 128);
+            mbar_init(bar_o(t), 1);
         }
-        mbar_init(bar_p, 128);
-        mbar_init(bar_o, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 5) {  // TMEM: S0 [0,128), S1 [128,256), O [256, 256+D)
+    if (warp == 9) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&bars->tmem_base))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -225,14 +256,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    const uint32_t tmem_o = tmem + 256;
 
-    if (warp == 4) {
-        // ============================ TMA producer ============================
-        if (lane == 0 && n_kt > 0) {
-            mbar_expect_tx(bar_q, (D / 64) * L::BOX);
-            for (int c = 0; c < D / 64; ++c)
-                tma_load_3d(sbase + L::Q_OFF + c * L::BOX, &tm_q, bar_q, c * 64, 0, row0 / g);
+    if (warp >= 8) {
+        setmaxnreg_dec_88();
+        if (warp == 8 && lane == 0 && n_kt > 0) {
+            // ============================ TMA producer ============================
+            mbar_expect_tx(bar_q, n_tiles * (D / 64) * L::BOX);
+            for (int tt = 0; tt < n_tiles; ++tt)
+                for (int c = 0; c < D / 64; ++c)
+                    tma_load_3d(sbase + L::Q_OFF + (tt * (D / 64) + c) * L::BOX, &tm_q, bar_q, c * 64, 0,
+                                (row0 + tt * BM) / g);
             for (int i = 0; i < n_kt; ++i) {
                 const int s = i % NS;
                 if (i >= NS) mbar_wait(bar_e(s), ((i / NS) - 1) & 1);
@@ -243,215 +276,211 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int c = 0; c < D / 64; ++c)
                     tma_load_2d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, i * BN);
             }
-        }
-    } else if (warp == 5) {
-        // ============================ MMA issuer ==============================
-        constexpr uint32_t ID_S = idesc_bf16(BM, BN, false);
-        constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
-        if (lane == 0 && n_kt > 0) {
+        } else if (warp == 9 && lane == 0 && n_kt > 0) {
+            // ============================ MMA issuer ==============================
+            constexpr uint32_t ID_S = idesc_bf16(BM, BN, false);
+            constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
+            const int nk_t[2] = {n_kt0, n_kt1};
             mbar_wait(bar_q, 0);
-            auto issue_s = [&](int i) {
-                const int s = i % NS, b = i & 1;
-                mbar_wait(bar_k(s), (i / NS) & 1);
-                if (i >= 2) mbar_wait(bar_sr(b), ((i - 2) >> 1) & 1);
-                tc_fence_after();
+            auto issue_s = [&](int tt, int i) {  // S_tt(i) = Q_tt K(i)^T
+                const int s = i % NS;
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t off = (ks >> 2) * L::BOX + (ks & 3) * 32;
-                    const uint64_t a = sdesc(sbase + L::Q_OFF + off, 16, 1024);
-                    const uint64_t bdesc = sdesc(sbase + L::K_OFF + s * (D / 64) * L::BOX + off, 16, 1024);
-                    umma_bf16(tmem + b * BN, a, bdesc, ID_S, ks > 0);
+                    const uint64_t a = sdesc(sbase + L::Q_OFF + tt * (D / 64) * L::BOX + off, 16, 1024);
+                    const uint64_t b = sdesc(sbase + L::K_OFF + s * (D / 64) * L::BOX + off, 16, 1024);
+                    umma_bf16(tmem + tt * 256, a, b, ID_S, ks > 0);
                 }
-                umma_commit(bar_sf(b));
+                umma_commit(bar_s(tt));
             };
-            issue_s(0);
-            for (int j = 0; j < n_kt; ++j) {
-                if (j + 1 < n_kt) issue_s(j + 1);
+            auto issue_pv = [&](int tt, int j) {  // O_tt += P_tt(j) V(j), P from TMEM
                 const int s = j % NS;
-                mbar_wait(bar_p, j & 1);
-                mbar_wait(bar_v(s), (j / NS) & 1);
-                tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk) {
-                    const uint64_t a = sdesc(sbase + L::P_OFF + (kk >> 2) * L::BOX + (kk & 3) * 32, 16, 1024);
-                    const uint64_t bdesc = sdesc(sbase + L::V_OFF + s * (D / 64) * L::BOX + kk * 16 * 128, L::BOX, 1024);
-                    umma_bf16(tmem_o, a, bdesc, ID_O, (j > 0 || kk > 0 || !first) ? 1u : 0u);
+                    const uint64_t b = sdesc(sbase + L::V_OFF + s * (D / 64) * L::BOX + kk * 16 * 128, L::BOX, 1024);
+                    umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, b, ID_O,
+                                 (j > 0 || kk > 0 || !first) ? 1u : 0u);
                 }
-                umma_commit(bar_e(s));
-                umma_commit(bar_o);
+                umma_commit(bar_o(tt));
+            };
+            mbar_wait(bar_k(0), 0);
+            tc_fence_after();
+            for (int tt = 0; tt < n_tiles; ++tt)
+                if (nk_t[tt] > 0) issue_s(tt, 0);
+            for (int j = 0; j < n_kt; ++j) {
+                const int s = j % NS;
+                bool waited_v = false, waited_k = false;
+                for (int tt = 0; tt < n_tiles; ++tt) {
+                    if (j >= nk_t[tt]) continue;
+                    mbar_wait(bar_p(tt), j & 1);
+                    if (!waited_v) { mbar_wait(bar_v(s), (j / NS) & 1); waited_v = true; }
+                    tc_fence_after();
+                    issue_pv(tt, j);
+                    if (j + 1 < nk_t[tt]) {
+                        if (!waited_k) { mbar_wait(bar_k((j + 1) % NS), ((j + 1) / NS) & 1); waited_k = true; }
+                        tc_fence_after();
+                        issue_s(tt, j + 1);
+                    }
+                }
+                umma_commit(bar_e(s));  // K(j), V(j) consumed by every tile
             }
         }
     } else {
-        // ====================== softmax / correction / epilogue (warps 0-3) ======================
-        const int r = warp * 32 + lane;           // tile row == TMEM lane
-        const int rg = row0 + r;                  // packed row index t*g + j
+        // ====================== softmax / correction / epilogue: warps 0-3 tile 0, 4-7 tile 1 ======================
+        setmaxnreg_inc_208();
+        const int tt = warp >> 2;
+        const int wq = warp & 3;                  // TMEM lane quarter
+        const int r = wq * 32 + lane;             // row within the tile == TMEM lane
+        const int rg = row0 + tt * BM + r;        // packed row index t*g + j
         const bool row_valid = rg < n_rows;
         const int t = row_valid ? rg / g : 0;
         const int64_t qpos = p.q_pos0 + t;
-        const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+        const int nkt = tt == 0 ? n_kt0 : n_kt1;
+        const int t_lo = (row0 + tt * BM) / g;
+        const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+        const uint32_t t_s = tmem + tt * 256 + lane_addr;        // S / P columns of this row
+        const uint32_t t_o = t_s + 128;                          // O columns of this row
         const float sc = p.scale_log2;
         float m_run = -CUDART_INF_F, l_run = 0.f;
-        if (!first) {
-            m_run = row_valid ? p.m_acc[rg] : -CUDART_INF_F;
-            l_run = row_valid ? p.l_acc[rg] : 0.f;
-            if (n_kt > 0) {  // running O -> TMEM before the first PV accumulates onto it
+        if (tt < n_tiles) {
+            if (!first) {
+                m_run = row_valid ? p.m_acc[rg] : -CUDART_INF_F;
+                l_run = row_valid ? p.l_acc[rg] : 0.f;
+                if (nkt > 0) {  // running O -> TMEM before the first PV accumulates onto it
 #pragma unroll
-                for (int cb = 0; cb < D / 32; ++cb) {
-                    uint32_t v[32];
-                    const float4* src = reinterpret_cast<const float4*>(p.o_acc + static_cast<int64_t>(row_valid ? rg : 0) * D + cb * 32);
+                    for (int cb = 0; cb < D / 32; ++cb) {
+                        uint32_t v[32];
+                        const float4* src = reinterpret_cast<const float4*>(p.o_acc + static_cast<int64_t>(row_valid ? rg : 0) * D + cb * 32);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        float4 f = row_valid ? src[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-                        v[4 * i] = __float_as_uint(f.x); v[4 * i + 1] = __float_as_uint(f.y);
-                        v[4 * i + 2] = __float_as_uint(f.z); v[4 * i + 3] = __float_as_uint(f.w);
+                        for (int i = 0; i < 8; ++i) {
+                            float4 f = row_valid ? src[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+                            v[4 * i] = __float_as_uint(f.x); v[4 * i + 1] = __float_as_uint(f.y);
+                            v[4 * i + 2] = __float_as_uint(f.z); v[4 * i + 3] = __float_as_uint(f.w);
+                        }
+                        tmem_st32(t_o + cb * 32, v);
                     }
-                    tmem_st32(tmem_o + lane_addr + cb * 32, v);
-                }
-                tmem_wait_st();
-            }
-        }
-        uint8_t* sP = smem + L::P_OFF;
-        for (int j = 0; j < n_kt; ++j) {
-            const int b = j & 1;
-            mbar_wait(bar_sf(b), (j >> 1) & 1);
-            tc_fence_after();
-            float x[BN];
-#pragma unroll
-            for (int cb = 0; cb < BN / 32; ++cb) {
-                uint32_t v[32];
-                tmem_ld32(tmem + b * BN + lane_addr + cb * 32, v);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) x[cb * 32 + i] = __uint_as_float(v[i]);
-            }
-            tc_fence_before();
-            mbar_arrive(bar_sr(b));  // S buffer b may be overwritten by S(j+2)
-            // mask: keys beyond the segment / not yet visible (causal)
-            const int key0 = j * BN;
-            const bool need_mask = (key0 + BN > n_k_eff) || (causal && p.k_pos0 + key0 + BN - 1 > p.q_pos0 + t_lo);
-            float mx = -CUDART_INF_F;
-            if (need_mask) {
-                const int64_t lim = qpos - p.k_pos0;  // key index visible iff key <= lim (causal)
-#pragma unroll
-                for (int i = 0; i < BN; ++i) {
-                    const int key = key0 + i;
-                    const bool vis = key < n_k_eff && (!causal || key <= lim);
-                    x[i] = vis ? x[i] * sc : -CUDART_INF_F;
-                    mx = fmaxf(mx, x[i]);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < BN; ++i) {
-                    x[i] *= sc;
-                    mx = fmaxf(mx, x[i]);
+                    tmem_wait_st();
                 }
             }
-            // lazy rescale: move the reference max only when it grows by > 2^8
-            float m_ref = m_run, alpha = 1.f;
-            const bool grow = mx > m_run + RESCALE_THRESHOLD || (m_run == -CUDART_INF_F && mx != -CUDART_INF_F);
-            if (grow) {
-                m_ref = mx;
-                alpha = (m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mx);
-            }
-            const float m_use = (m_ref == -CUDART_INF_F) ? 0.f : m_ref;
-            float lsum = 0.f;
-#pragma unroll
-            for (int i = 0; i < BN; ++i) {
-                x[i] = ex2(x[i] - m_use);
-                lsum += x[i];
-            }
-            // PV(j-1) must be complete before P is overwritten / O is corrected
-            if (j > 0) {
-                mbar_wait(bar_o, (j - 1) & 1);
+            for (int j = 0; j < nkt; ++j) {
+                mbar_wait(bar_s(tt), j & 1);   // also implies PV(j-1) of this tile is complete (in-order MMAs)
                 tc_fence_after();
-            }
-            const bool o_live = !first || j > 0;
-            if (o_live && __any_sync(0xffffffffu, grow)) {
+                uint32_t x[BN];
 #pragma unroll
-                for (int cb = 0; cb < D / 32; ++cb) {
-                    uint32_t v[32];
-                    tmem_ld32(tmem_o + lane_addr + cb * 32, v);
-                    tmem_wait_ld();
+                for (int cb = 0; cb < BN / 32; ++cb)
+                    tmem_ld32(t_s + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[cb * 32]));
+                tmem_wait_ld();
+                // row max of the raw scores (scale > 0 commutes with max); masking where needed
+                const int key0 = j * BN;
+                const bool need_mask = (key0 + BN > p.n_k) || (causal && p.k_pos0 + key0 + BN - 1 > p.q_pos0 + t_lo);
+                float mx = -CUDART_INF_F;
+                if (need_mask) {
+                    const int64_t lim = causal ? qpos - p.k_pos0 : static_cast<int64_t>(p.n_k) - 1;
+                    const int64_t lim2 = lim < p.n_k - 1 ? lim : static_cast<int64_t>(p.n_k) - 1;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-                    tmem_st32(tmem_o + lane_addr + cb * 32, v);
-                }
-                tmem_wait_st();
-            }
-            l_run = l_run * alpha + lsum;
-            m_run = m_ref;
-            // P (bf16) -> SMEM, K-major SWIZZLE_128B: row r, 16-byte chunk c of 64-key block kb
-#pragma unroll
-            for (int kb = 0; kb < BN / 64; ++kb) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float* xs = x + kb * 64 + c * 8;
-                    uint4 w;
-                    w.x = pack_bf16(xs[0], xs[1]);
-                    w.y = pack_bf16(xs[2], xs[3]);
-                    w.z = pack_bf16(xs[4], xs[5]);
-                    w.w = pack_bf16(xs[6], xs[7]);
-                    *reinterpret_cast<uint4*>(sP + kb * L::BOX + r * 128 + ((c ^ (r & 7)) << 4)) = w;
-                }
-            }
-            fence_async_smem();
-            tc_fence_before();
-            mbar_arrive(bar_p);
-        }
-        // ---- epilogue ----
-        if (n_kt > 0) {
-            mbar_wait(bar_o, (n_kt - 1) & 1);
-            tc_fence_after();
-        }
-        if (last) {
-            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-            __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (rg % g) * D;
-#pragma unroll
-            for (int cb = 0; cb < D / 32; ++cb) {
-                uint32_t v[32];
-                if (n_kt > 0) {
-                    tmem_ld32(tmem_o + lane_addr + cb * 32, v);
-                    tmem_wait_ld();
+                    for (int i = 0; i < BN; ++i) {
+                        if (key0 + i > lim2) x[i] = __float_as_uint(-CUDART_INF_F);
+                        mx = fmaxf(mx, __uint_as_float(x[i]));
+                    }
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        v[i] = (row_valid && !first) ? __float_as_uint(p.o_acc[static_cast<int64_t>(rg) * D + cb * 32 + i]) : 0u;
+                    for (int i = 0; i < BN; ++i) mx = fmaxf(mx, __uint_as_float(x[i]));
                 }
-                if (row_valid) {
+                const float mxs = mx * sc;  // log2-domain tile max
+                // lazy rescale: move the reference max only when it grows by > 2^8
+                float m_ref = m_run, alpha = 1.f;
+                const bool grow = (mx != -CUDART_INF_F) && (m_run == -CUDART_INF_F || mxs > m_run + RESCALE_THRESHOLD);
+                if (grow) {
+                    m_ref = mxs;
+                    alpha = (m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mxs);
+                }
+                const float neg_m = (m_ref == -CUDART_INF_F) ? 0.f : -m_ref;
+                float lsum0 = 0.f, lsum1 = 0.f;
+                // p = 2^(x*scale - m): packed to bf16 pairs in place (x[i/2] is dead once read)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        uint4 w;
-                        w.x = pack_bf16(__uint_as_float(v[8 * i]) * inv, __uint_as_float(v[8 * i + 1]) * inv);
-                        w.y = pack_bf16(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv);
-                        w.z = pack_bf16(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv);
-                        w.w = pack_bf16(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv);
-                        *reinterpret_cast<uint4*>(dst + cb * 32 + 8 * i) = w;
+                for (int i = 0; i < BN; i += 2) {
+                    const float p0 = ex2(fmaf(__uint_as_float(x[i]), sc, neg_m));
+                    const float p1 = ex2(fmaf(__uint_as_float(x[i + 1]), sc, neg_m));
+                    lsum0 += p0;
+                    lsum1 += p1;
+                    x[i / 2] = pack_bf16(p0, p1);
+                }
+                // P -> TMEM (overwrites the consumed S columns of this row)
+                tmem_st32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));
+                const bool o_live = !first || j > 0;
+                if (o_live && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+                    for (int cb = 0; cb < D / 32; ++cb) {
+                        uint32_t v[32];
+                        tmem_ld32(t_o + cb * 32, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+                        tmem_st32(t_o + cb * 32, v);
                     }
                 }
+                tmem_wait_st();
+                l_run = l_run * alpha + (lsum0 + lsum1);
+                m_run = m_ref;
+                tc_fence_before();
+                mbar_arrive(bar_p(tt));
             }
-        } else if (n_kt > 0) {
+            // ---- epilogue ----
+            if (nkt > 0) {
+                mbar_wait(bar_o(tt), (nkt - 1) & 1);
+                tc_fence_after();
+            }
+            if (last) {
+                const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (rg % g) * D;
 #pragma unroll
-            for (int cb = 0; cb < D / 32; ++cb) {
-                uint32_t v[32];
-                tmem_ld32(tmem_o + lane_addr + cb * 32, v);
-                tmem_wait_ld();
-                if (row_valid) {
-                    float4* dst = reinterpret_cast<float4*>(p.o_acc + static_cast<int64_t>(rg) * D + cb * 32);
+                for (int cb = 0; cb < D / 32; ++cb) {
+                    uint32_t v[32];
+                    if (nkt > 0) {
+                        tmem_ld32(t_o + cb * 32, v);
+                        tmem_wait_ld();
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                             __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                        for (int i = 0; i < 32; ++i)
+                            v[i] = (row_valid && !first) ? __float_as_uint(p.o_acc[static_cast<int64_t>(rg) * D + cb * 32 + i]) : 0u;
+                    }
+                    if (row_valid) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            uint4 w;
+                            w.x = pack_bf16(__uint_as_float(v[8 * i]) * inv, __uint_as_float(v[8 * i + 1]) * inv);
+                            w.y = pack_bf16(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv);
+                            w.z = pack_bf16(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv);
+                            w.w = pack_bf16(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv);
+                            *reinterpret_cast<uint4*>(dst + cb * 32 + 8 * i) = w;
+                        }
+                    }
                 }
-            }
-            if (row_valid) {
-                p.m_acc[rg] = m_run;
-                p.l_acc[rg] = l_run;
+            } else if (nkt > 0) {
+#pragma unroll
+                for (int cb = 0; cb < D / 32; ++cb) {
+                    uint32_t v[32];
+                    tmem_ld32(t_o + cb * 32, v);
+                    tmem_wait_ld();
+                    if (row_valid) {
+                        float4* dst = reinterpret_cast<float4*>(p.o_acc + static_cast<int64_t>(rg) * D + cb * 32);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                    }
+                }
+                if (row_valid) {
+                    p.m_acc[rg] = m_run;
+                    p.l_acc[rg] = l_run;
+                }
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == 9) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
@@ -488,7 +517,7 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
 template <int D>
 cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
     const int n_rows = p.n_q * p.g;
-    const int grid = (n_rows + BM - 1) / BM;
+    const int grid = (n_rows + 2 * BM - 1) / (2 * BM);
     if (grid == 0) return cudaSuccess;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
