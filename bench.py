@@ -3,7 +3,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload auto|8B-1M|8B-128K|tiny]
 
 A "step" (ours): one pass of the hot path over one batch of synthetic input --
-  prefill step = one 16384-token chunk through all 32 layers (write-back D2H, history H2D through
+  prefill step = one 18944-token chunk (148 SMs x 256 rows / g) through all 32 layers (write-back D2H, history H2D through
                  the staging slots, causal attention over history + chunk, per layer call);
                  the timed chunks are the LAST K chunks of the 1M prefill (the most expensive ones),
                  the W warm-up chunks precede them; the history before them is placed in the host
@@ -33,9 +33,11 @@ sys.path.insert(0, ROOT)
 METRIC = "1M-ctx Llama-3-8B-shape prefill tok/s, decode ms/tok; H2D GB/s vs link peak"
 WORKLOADS = {
     # name: (layers, q_heads, kv_heads, d, context S, chunk)
-    "8B-1M": (32, 32, 8, 128, 1 << 20, 16384),
-    "8B-128K": (32, 32, 8, 128, 131072, 16384),
-    "tiny": (1, 4, 2, 64, 1024, 256),
+    # chunk = 148 SMs x 256 rows (two 128-row Q tiles per CTA) / g = 18944 tokens for g = 4: every
+    # prefill launch is exactly 2 full waves (16384 would leave a 73%-full second wave)
+    "8B-1M": (32, 32, 8, 128, 1 << 20, 18944),
+    "8B-128K": (32, 32, 8, 128, 131072, 18944),
+    "tiny": (1, 4, 2, 64, 1024, 128),
 }
 SEED = 0x48454144
 DIST = "U"  # throughput workload

@@ -7,7 +7,7 @@ from synth.cuda import fill_
 
 ctxlen = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-c = 16384
+c = int(sys.argv[3]) if len(sys.argv) > 3 else 18944
 t0 = time.time()
 hi = HeadInfer(L, 32, 8, 128, ctxlen + 128, c)
 print(f"init {time.time()-t0:.1f}s stats={hi.stats()}", flush=True)
