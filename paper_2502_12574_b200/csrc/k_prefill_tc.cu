@@ -39,6 +39,7 @@ constexpr int BN = 128;            // keys per KV tile
 constexpr int NS = 2;              // K/V pipeline stages
 constexpr int NUM_THREADS = 384;   // 2 x 4 softmax warps (one Q tile each) + TMA warp + MMA warp + 2 spare
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+constexpr int EX2_POLY_EVERY = 16;         // 2 of every 16 exponentials on the FMA pipe (see ex2_poly)
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -145,6 +146,19 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+// 2^x on the FMA/ALU pipes (round-to-nearest split + degree-3 fit on [-0.5, 0.5], rel. err < 8e-5,
+// far below the bf16 rounding P undergoes): relieves the MUFU unit, which the softmax otherwise
+// saturates at the same rate the tensor core consumes P.  Inputs below -126 return ~2^-126 (a denormal, below every bf16 P that matters).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -126.f);  // keeps the exponent field >= 0 for every p in [0.707, 1.415)
+    const float t = x + 12582912.f;           // 1.5 * 2^23: round(x) lands in the low mantissa bits
+    const float n = t - 12582912.f;
+    const float f = x - n;                    // f in [-0.5, 0.5]
+    float p = fmaf(5.5160172e-2f, f, 2.4258254e-1f);
+    p = fmaf(p, f, 6.9326055e-1f);
+    p = fmaf(p, f, 9.9993026e-1f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
@@ -373,19 +387,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 // row max of the raw scores (scale > 0 commutes with max); masking where needed
                 const int key0 = j * BN;
                 const bool need_mask = (key0 + BN > p.n_k) || (causal && p.k_pos0 + key0 + BN - 1 > p.q_pos0 + t_lo);
-                float mx = -CUDART_INF_F;
                 if (need_mask) {
                     const int64_t lim = causal ? qpos - p.k_pos0 : static_cast<int64_t>(p.n_k) - 1;
                     const int64_t lim2 = lim < p.n_k - 1 ? lim : static_cast<int64_t>(p.n_k) - 1;
 #pragma unroll
-                    for (int i = 0; i < BN; ++i) {
+                    for (int i = 0; i < BN; ++i)
                         if (key0 + i > lim2) x[i] = __float_as_uint(-CUDART_INF_F);
-                        mx = fmaxf(mx, __uint_as_float(x[i]));
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < BN; ++i) mx = fmaxf(mx, __uint_as_float(x[i]));
                 }
+                // 8 independent max chains (short dependency chain), then combine
+                float mk[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) mk[c] = __uint_as_float(x[c]);
+#pragma unroll
+                for (int i = 8; i < BN; i += 8)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) mk[c] = fmaxf(mk[c], __uint_as_float(x[i + c]));
+                float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])), fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
                 const float mxs = mx * sc;  // log2-domain tile max
                 // lazy rescale: move the reference max only when it grows by > 2^8
                 float m_ref = m_run, alpha = 1.f;
@@ -395,16 +412,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     alpha = (m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mxs);
                 }
                 const float neg_m = (m_ref == -CUDART_INF_F) ? 0.f : -m_ref;
-                float lsum0 = 0.f, lsum1 = 0.f;
-                // p = 2^(x*scale - m): packed to bf16 pairs in place (x[i/2] is dead once read)
+                float ls[4] = {0.f, 0.f, 0.f, 0.f};
+                // p = 2^(x*scale - m): packed to bf16 pairs in place (x[i/2] is dead once read).  One
+                // element in EX2_POLY_EVERY goes through the FMA-pipe polynomial, the rest through MUFU.
 #pragma unroll
                 for (int i = 0; i < BN; i += 2) {
-                    const float p0 = ex2(fmaf(__uint_as_float(x[i]), sc, neg_m));
-                    const float p1 = ex2(fmaf(__uint_as_float(x[i + 1]), sc, neg_m));
-                    lsum0 += p0;
-                    lsum1 += p1;
+                    const float a0 = fmaf(__uint_as_float(x[i]), sc, neg_m);
+                    const float a1 = fmaf(__uint_as_float(x[i + 1]), sc, neg_m);
+                    const float p0 = ((i % EX2_POLY_EVERY) == EX2_POLY_EVERY - 2) ? ex2_poly(a0) : ex2(a0);
+                    const float p1 = (((i + 1) % EX2_POLY_EVERY) == EX2_POLY_EVERY - 1) ? ex2_poly(a1) : ex2(a1);
+                    ls[(i >> 1) & 3] += p0 + p1;
                     x[i / 2] = pack_bf16(p0, p1);
                 }
+                const float lsum0 = (ls[0] + ls[1]), lsum1 = (ls[2] + ls[3]);
                 // P -> TMEM (overwrites the consumed S columns of this row)
                 tmem_st32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
                 tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));

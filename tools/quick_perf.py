@@ -16,8 +16,9 @@ buf_k = torch.empty((c, 1, 128), dtype=torch.bfloat16, device="cuda"); buf_v = t
 for l in range(L):
     for h in range(8):
         for p0 in range(0, ctxlen, c):
-            fill_(buf_k, 1, 1, "U", l, h, p0); fill_(buf_v, 1, 2, "U", l, h, p0)
-            hi.write_host_kv(l, h, p0, buf_k[:, 0], buf_v[:, 0])
+            n = min(c, ctxlen - p0)
+            fill_(buf_k[:n], 1, 1, "U", l, h, p0); fill_(buf_v[:n], 1, 2, "U", l, h, p0)
+            hi.write_host_kv(l, h, p0, buf_k[:n, 0], buf_v[:n, 0])
 print(f"fill {time.time()-t0:.1f}s", flush=True)
 s = ctxlen - c
 Q = fill_(torch.empty((c, 32, 128), dtype=torch.bfloat16, device="cuda"), 1, 0, "U", 0, 0, s)
