@@ -160,7 +160,7 @@ def run_ours(args, rank, world, local_rank, pg):
     wl = pick_workload(args.workload, world, K, W)
     if world > 1:
         # every rank must agree on the workload
-        t = torch.tensor([list(WORKLOADS).index(wl)], device="cuda")
+        t = torch.tensor([list(WORKLOADS).index(wl)], device="cpu" if args.ranks_share_gpu else "cuda")
         dist.broadcast(t, 0)
         wl = list(WORKLOADS)[int(t.item())]
     L, hq, hkv, d, S, c = WORKLOADS[wl]
@@ -174,8 +174,14 @@ def run_ours(args, rank, world, local_rank, pg):
     peaks = rf.load_peaks()
     shape = rf.Shape(L, hq, hkv, d)
 
+    resident = args.resident_heads
+    if resident < 0:  # as many (layer, kv head) pairs as fit next to this bench's inputs (NEXT-1)
+        free_b, _ = torch.cuda.mem_get_info()
+        inputs_b = (K + 2) * L * c * (hq_loc + 2 * hkv_loc) * d * 2 + L * c * hq_loc * d * 2
+        pair_b = 4 * d * max_ctx
+        resident = int(max(0, min(L * hkv_loc, (free_b - inputs_b - (10 << 30)) // pair_b)))
     t0 = time.time()
-    hi = HeadInfer(L, hq, hkv, d, max_ctx, c, rank, world, flags=HI_FLAG_TIMING)
+    hi = HeadInfer(L, hq, hkv, d, max_ctx, c, rank, world, flags=HI_FLAG_TIMING, resident_kv_heads=resident)
     init_s = time.time() - t0
     t0 = time.time()
     fill_history(hi, L, hkv_loc, kv0h, d, s0, torch, fill_)
@@ -192,13 +198,18 @@ def run_ours(args, rank, world, local_rank, pg):
         if world > 1:
             dist.barrier(group=pg)
 
+    gathered0 = None
+
     def prefill_step(inputs, outs):
-        nonlocal gathered
+        nonlocal gathered, gathered0
         for l in range(L):
             Q, Kt, Vt = inputs[l]
             hi.prefill_chunk(l, Q, Kt, Vt, outs[l])
             if world > 1:
-                gathered = gather_heads(outs[l], group=pg, out=gathered)
+                if l == 0:
+                    gathered0 = gather_heads(outs[l], group=pg, out=gathered0)
+                else:
+                    gathered = gather_heads(outs[l], group=pg, out=gathered)
 
     # ---------------- prefill: W warm-up chunks, then K timed chunks (all inputs resident) -------
     outs = [torch.empty((c, hq_loc, d), dtype=torch.bfloat16, device="cuda") for _ in range(L)]
@@ -296,7 +307,8 @@ def run_ours(args, rank, world, local_rank, pg):
         e2e = {"ms": e2e_ms, "h2d": h2d_b, "d2h": d2h_b}
 
     # ---------------- max over ranks --------------------------------------------------------------
-    times = torch.tensor([pre_ms, dec_ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64, device="cuda")
+    times = torch.tensor([pre_ms, dec_ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64,
+                         device="cpu" if args.ranks_share_gpu else "cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX, group=pg)
     pre_ms, dec_ms, e2e_ms = times.tolist()
@@ -371,11 +383,14 @@ def run_ours(args, rank, world, local_rank, pg):
         "clocks": clk,
         "gpu_launches": launches,
         "residency": {"staging_bytes": st1["staging_bytes"], "one_head_bytes": st1["staging_bound_bytes"],
-                      "host_store_bytes": st1["host_store_bytes"], "init_s": round(init_s, 2)},
+                      "host_store_bytes": st1["host_store_bytes"], "init_s": round(init_s, 2),
+                      "resident_kv_heads": st1["resident_kv_heads"], "resident_bytes": st1["resident_bytes"]},
     }
     if e2e:
         res["e2e"] = {"value": round(K * c / (e2e_ms / 1e3), 2), "unit": "tok/s",
                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
+    if world > 1 and not args.no_cpu_baseline:
+        res["parity_sample"] = sharded_parity(gathered0, last_chunk_pos, L, hq, hkv, d, world, torch)
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"], res["parity_sample"] = cpu_baseline(hi, sample_out0, last_chunk_pos, dec_sample, dec_pos,
                                                                  L, hq, hkv, d, torch)
@@ -415,17 +430,13 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
         toks = np.unique(np.concatenate([[0, c - 1], rng.integers(0, c, max(0, n_tok - 2))]))[:n_tok]
         return toks
 
+    # calibrate on one call of `cores` rows (the oracle parallelises over the rows of a call)
+    k0, v0 = kv[heads[0]]
+    probe_t = rows_for(cores)
     t0 = time.time()
-    probe_t = rows_for(max(1, cores // (g * len(heads))) or 1)
-    n_rows = 0
-    for h in heads:
-        k, v = kv[h]
-        for j in range(h * g, (h + 1) * g):
-            oracle.attention_rows(qpre[probe_t, j], chunk_pos + probe_t, k, v)
-            n_rows += len(probe_t)
-    probe_s = time.time() - t0
-    per_row = probe_s / max(n_rows, 1)
-    n_tok = int(max(2, min(c, budget_s / max(per_row, 1e-9) / (g * len(heads)))))
+    oracle.attention_rows(qpre[probe_t, 0], chunk_pos + probe_t, k0, v0)
+    rows_per_s = len(probe_t) / max(time.time() - t0, 1e-9)
+    n_tok = int(max(2, min(c, budget_s * rows_per_s / (g * len(heads)))))
     toks = rows_for(n_tok)
     t0 = time.time()
     maxerr, sumerr, cnt, rows = 0.0, 0.0, 0, 0
@@ -457,6 +468,29 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
     parity = {"prefill_rows": rows, "prefill_max_abs": maxerr, "prefill_mean_abs": sumerr / max(cnt, 1),
               "decode_rows": len(heads) * g, "decode_max_abs": dmax, "tol_max_abs": 2e-2, "tol_mean_abs": 2e-3}
     return cpu, parity
+
+
+def sharded_parity(gathered0, chunk_pos, L, hq, hkv, d, world, torch, n_tok=4):
+    """Head-sharded run: rows of the all-gathered layer-0 output of the last timed chunk, one q head
+    per rank, against the oracle (checks the shard arithmetic + the collective end to end)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    from paper_2502_12574_b200.parallel import to_token_major
+    oracle.build()
+    full = to_token_major(gathered0).float().cpu().numpy()  # [c, hq, d]
+    c = full.shape[0]
+    g = hq // hkv
+    toks = np.array([0, c // 3, 2 * c // 3, c - 1][:n_tok])
+    maxerr = 0.0
+    for r in range(world):
+        j = r * (hq // world)          # first q head owned by rank r
+        kv, v = _oracle_inputs_for_head(0, j // g, chunk_pos + c, d, torch)
+        q = synth.gen_block(SEED, 0, DIST, 0, j, 1, chunk_pos, c, d)[toks, 0]
+        ref = oracle.attention_rows(q, chunk_pos + toks, kv, v)
+        maxerr = max(maxerr, float(np.abs(full[toks, j] - ref).max()))
+    return {"gathered_rows": int(len(toks) * world), "max_abs": maxerr, "tol_max_abs": 2e-2}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -522,6 +556,10 @@ def main():
     ap.add_argument("--workload", choices=["auto"] + list(WORKLOADS), default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--resident-heads", type=int, default=0,
+                    help="NEXT-1: keep the first R (layer, kv head) pairs' KV in HBM (-1 = as many as fit)")
+    ap.add_argument("--ranks-share-gpu", action="store_true",
+                    help="validation only: every rank uses cuda:0 and the output gather goes through gloo")
     args = ap.parse_args()
     if args.warmup < 3:
         log("bench: warmup < 3 is not a valid measurement; using 3")
@@ -534,10 +572,15 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    if args.ranks_share_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     pg = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.ranks_share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         pg = dist.group.WORLD
     try:
         run_ours(args, rank, world, local_rank, pg)

@@ -62,7 +62,14 @@ typedef struct hi_options {
     int numa_policy;      /* 0 = bind the host store to the GPU's NUMA node (sysfs), 1 = no binding,
                              2 = bind to numa_node */
     int numa_node;        /* used when numa_policy == 2 */
+    int resident_kv_heads; /* NEXT-1 (Alg. 1 H_on, l.1 and l.7-8 / l.22-23): the first R (layer,
+                              local kv head) pairs in layer-major order keep their whole KV cache in HBM
+                              (2*max_ctx*head_dim bf16 each) -- updated in place, never offloaded, attended
+                              straight from HBM; the rest are offloaded as usual.  0 (default) = pure head-
+                              wise offload; HI_RESIDENT_AUTO = as many pairs as fit in free HBM minus ~12 GiB */
 } hi_options;
+
+#define HI_RESIDENT_AUTO (-1)
 
 #define HI_FLAG_POISON_SLOTS 0x1 /* fill each staging slot with NaN before every H2D (race detection) */
 #define HI_FLAG_NO_HUGEPAGE 0x2  /* do not madvise(MADV_HUGEPAGE) the host store */
@@ -93,6 +100,8 @@ typedef struct hi_stats {
     int numa_node;                /* node the host store is bound to (-1: none / unknown) */
     int n_slots;
     int64_t slot_tokens;
+    int resident_kv_heads;        /* H_on pairs held in HBM (NEXT-1) */
+    int64_t resident_bytes;       /* their device KV bytes */
 } hi_stats;
 
 /*
@@ -145,8 +154,9 @@ hi_status hi_free(hi_ctx* ctx);
 
 /* ---- verification / introspection / bench preparation (not on the hot path) ---- */
 
-/* Copy host KV rows [pos, pos+n) of (layer, local kv head) into host buffers k_dst, v_dst
- * ([n, head_dim] bf16 each).  Waits for pending write-backs first.  HI_ESHAPE on bad range. */
+/* Copy KV rows [pos, pos+n) of (layer, local kv head) into host buffers k_dst, v_dst ([n, head_dim]
+ * bf16 each) from wherever they live (host store, or HBM for resident pairs).  Waits for pending
+ * write-backs first.  HI_ESHAPE on bad range. */
 hi_status hi_read_host_kv(hi_ctx* ctx, int layer, int kv_head_local, int64_t pos, int64_t n,
                           void* k_dst, void* v_dst);
 

@@ -18,6 +18,7 @@ HI_FLAG_NO_HUGEPAGE = 0x2
 HI_FLAG_SERIALIZE = 0x4
 HI_FLAG_TIMING = 0x8
 HI_FLAG_MMA_SYNC_PREFILL = 0x10
+HI_RESIDENT_AUTO = -1
 
 # every symbol include/headinfer.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",
@@ -27,7 +28,8 @@ EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", 
 
 class hi_options(ctypes.Structure):
     _fields_ = [("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64), ("device", ctypes.c_int),
-                ("flags", ctypes.c_int), ("numa_policy", ctypes.c_int), ("numa_node", ctypes.c_int)]
+                ("flags", ctypes.c_int), ("numa_policy", ctypes.c_int), ("numa_node", ctypes.c_int),
+                ("resident_kv_heads", ctypes.c_int)]
 
 
 class hi_stats(ctypes.Structure):
@@ -40,7 +42,8 @@ class hi_stats(ctypes.Structure):
                 ("prefill_attn_launches", ctypes.c_int64), ("decode_attn_ms", ctypes.c_double),
                 ("decode_attn_bytes", ctypes.c_double), ("decode_attn_launches", ctypes.c_int64),
                 ("init_seconds", ctypes.c_double),
-                ("numa_node", ctypes.c_int), ("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64)]
+                ("numa_node", ctypes.c_int), ("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64),
+                ("resident_kv_heads", ctypes.c_int), ("resident_bytes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

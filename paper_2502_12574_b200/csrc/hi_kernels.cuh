@@ -58,7 +58,9 @@ struct DecodeCombineParams {
     const __nv_bfloat16* v_new;  // [Hkv_loc][d]
     const float* parts;          // [Hkv_loc][max_parts][g][d+4]
     int max_parts;
-    int n_parts;                 // parts per kv head filled by this call (same for every head)
+    int n_parts;                 // parts per kv head for local kv heads h >= h_lo (offloaded)
+    int n_parts_lo;              // parts per kv head for h < h_lo (HBM-resident heads, NEXT-1)
+    int h_lo;
     int g;
     float scale_log2;
     __nv_bfloat16* out;          // [Hq_loc][d]

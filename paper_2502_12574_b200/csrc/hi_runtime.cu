@@ -63,7 +63,10 @@ struct hi_ctx {
     std::vector<int64_t> seq_len;
     bool sticky = false;
     std::string err = "no error";
-    // (a) host KV store
+    // (a) host KV store (offloaded pairs) + device-resident KV cache (H_on pairs, NEXT-1)
+    int n_res = 0;                     // (layer, kv head) pairs in layer-major order < n_res stay in HBM
+    uint8_t* d_res = nullptr;
+    size_t res_bytes = 0;
     uint8_t* host = nullptr;
     size_t host_bytes = 0;
     size_t host_map_bytes = 0;
@@ -99,14 +102,28 @@ struct hi_ctx {
     double prefill_ms = 0, prefill_flops = 0, decode_ms = 0, decode_bytes = 0;
     int64_t prefill_timed = 0, decode_timed = 0;
 
+    size_t pair(int layer, int h) const { return static_cast<size_t>(layer) * Hkv_loc + h; }
+    bool resident(int layer, int h) const { return pair(layer, h) < static_cast<size_t>(n_res); }
+    int resident_heads_of_layer(int layer) const {  // resident pairs of a layer are its first heads
+        return std::max(0, std::min(Hkv_loc, n_res - layer * Hkv_loc));
+    }
     uint8_t* host_k(int layer, int h, int64_t row) const {
-        return host + ((static_cast<size_t>(layer) * Hkv_loc + h) * 2 + 0) * static_cast<size_t>(max_ctx) * d * 2 +
+        return host + ((pair(layer, h) - n_res) * 2 + 0) * static_cast<size_t>(max_ctx) * d * 2 +
                static_cast<size_t>(row) * d * 2;
     }
     uint8_t* host_v(int layer, int h, int64_t row) const {
-        return host + ((static_cast<size_t>(layer) * Hkv_loc + h) * 2 + 1) * static_cast<size_t>(max_ctx) * d * 2 +
+        return host + ((pair(layer, h) - n_res) * 2 + 1) * static_cast<size_t>(max_ctx) * d * 2 +
                static_cast<size_t>(row) * d * 2;
     }
+    uint8_t* dev_k(int layer, int h, int64_t row) const {
+        return d_res + (pair(layer, h) * 2 + 0) * static_cast<size_t>(max_ctx) * d * 2 + static_cast<size_t>(row) * d * 2;
+    }
+    uint8_t* dev_v(int layer, int h, int64_t row) const {
+        return d_res + (pair(layer, h) * 2 + 1) * static_cast<size_t>(max_ctx) * d * 2 + static_cast<size_t>(row) * d * 2;
+    }
+    // where the KV rows of (layer, h) live: device cache (resident) or host store (offloaded)
+    uint8_t* kv_k(int layer, int h, int64_t row) const { return resident(layer, h) ? dev_k(layer, h, row) : host_k(layer, h, row); }
+    uint8_t* kv_v(int layer, int h, int64_t row) const { return resident(layer, h) ? dev_v(layer, h, row) : host_v(layer, h, row); }
     uint8_t* slot_k(int s) const { return d_stage + static_cast<size_t>(s) * slot_bytes; }
     uint8_t* slot_v(int s) const { return slot_k(s) + static_cast<size_t>(slot_tokens) * d * 2; }
 };
@@ -160,6 +177,7 @@ int numa_node_count() {
 // (a) host KV store: mmap + THP + mbind + parallel first touch + cudaHostRegister
 hi_status alloc_host_store(hi_ctx* c, int numa_policy, int numa_node_req) {
     const size_t huge = 2u << 20;
+    if (c->host_bytes == 0) return HI_OK;  // every pair resident in HBM
     c->host_map_bytes = (c->host_bytes + huge - 1) / huge * huge;
     void* p = mmap(nullptr, c->host_map_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
     if (p == MAP_FAILED) return set_err(c, HI_ENOMEM_HOST, "mmap of the host KV store failed");
@@ -223,6 +241,7 @@ void destroy(hi_ctx* c) {
     cudaFree(c->d_lacc);
     cudaFree(c->d_parts);
     cudaFree(c->d_kvnew);
+    cudaFree(c->d_res);
     if (c->host) {
         if (c->host_registered) cudaHostUnregister(c->host);
         munmap(c->host, c->host_map_bytes);
@@ -231,9 +250,10 @@ void destroy(hi_ctx* c) {
     delete c;
 }
 
-// Split length for the decode partial kernel: ~2 CTAs per SM per history block.
+// Split length for the decode partial kernel (one 288-thread CTA per SM, TMA-fed ring): ~2 waves of
+// CTAs per history block, at least 64 keys (one ring stage) per CTA.
 int decode_split_len(int64_t nk) {
-    int64_t s = (nk + 295) / 296;
+    int64_t s = (nk + 2 * 148 - 1) / (2 * 148);
     s = (s + 63) / 64 * 64;
     return static_cast<int>(std::max<int64_t>(64, std::min<int64_t>(s, 1 << 20)));
 }
@@ -375,8 +395,8 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     hi_options o{};
     if (opt) o = *opt;
     if (o.n_slots == 0) o.n_slots = 4;
-    if (o.n_slots < 2 || o.n_slots > 64 || o.slot_tokens < 0) {
-        g_init_error = "invalid hi_options (n_slots in [2,64], slot_tokens >= 0)";
+    if (o.n_slots < 2 || o.n_slots > 64 || o.slot_tokens < 0 || o.resident_kv_heads < HI_RESIDENT_AUTO) {
+        g_init_error = "invalid hi_options (n_slots in [2,64], slot_tokens >= 0, resident_kv_heads >= -1)";
         return HI_EINVAL;
     }
 
@@ -410,8 +430,24 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess && prop.major < 10)
         return bail(HI_ECUDA, "libheadinfer is built for sm_100a (B200); device compute capability < 10");
 
-    // (a) host store
-    c->host_bytes = static_cast<size_t>(layers) * c->Hkv_loc * 2 * static_cast<size_t>(max_ctx) * head_dim * 2;
+    // (a) residency (NEXT-1, Alg. 1 H_on): the first n_res (layer, kv head) pairs keep their KV in HBM
+    const int n_pairs = layers * c->Hkv_loc;
+    const size_t pair_bytes = 2 * static_cast<size_t>(max_ctx) * head_dim * 2;
+    if (o.resident_kv_heads == HI_RESIDENT_AUTO) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); free_b = 0; }
+        const size_t reserve = (size_t(12) << 30) + c->slot_bytes * c->n_slots;  // workspaces + caller tensors
+        c->n_res = free_b > reserve ? static_cast<int>(std::min<size_t>(n_pairs, (free_b - reserve) / pair_bytes)) : 0;
+    } else {
+        c->n_res = std::min(o.resident_kv_heads, n_pairs);
+    }
+    c->res_bytes = static_cast<size_t>(c->n_res) * pair_bytes;
+    if (c->n_res > 0 && cudaMalloc(reinterpret_cast<void**>(&c->d_res), c->res_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(HI_ENOMEM_DEV, "cudaMalloc of the resident KV cache failed");
+    }
+    // (a) host store for the offloaded pairs
+    c->host_bytes = static_cast<size_t>(n_pairs - c->n_res) * pair_bytes;
     hi_status hs = alloc_host_store(c, o.numa_policy, o.numa_node);
     if (hs != HI_OK) return bail(hs, "");
 
@@ -424,7 +460,8 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
         return bail(HI_ENOMEM_DEV, "cudaMalloc of the staging slots failed");
     const size_t rows = static_cast<size_t>(chunk) * g;
     const int64_t max_blocks = (max_ctx + st - 1) / st;
-    c->max_parts = static_cast<int>(max_blocks * decode_parts_for_block(std::min<int64_t>(st, max_ctx)) + 8);
+    c->max_parts = static_cast<int>(std::max<int64_t>(max_blocks * decode_parts_for_block(std::min<int64_t>(st, max_ctx)),
+                                                     decode_parts_for_block(max_ctx)) + 8);
     const size_t pack_b = static_cast<size_t>(c->Hkv_loc) * 2 * chunk * head_dim * 2;
     const size_t oacc_b = rows * head_dim * 4, ml_b = rows * 4;
     const size_t parts_b = static_cast<size_t>(c->Hkv_loc) * c->max_parts * g * (head_dim + 4) * 4;
@@ -484,12 +521,18 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     HI_CK(c, cudaEventRecord(c->ev_packed, c->s_comp));
     // history H2D of this layer must see every earlier write-back of its rows (RAW via host DRAM)
     HI_CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_layer_d2h[layer], 0));
-    // write-back (Alg. 1 line 11): D2H of the chunk's rows [s, s+n) of every local kv head
+    // write-back (Alg. 1 line 11): D2H of the chunk's rows [s, s+n) of every offloaded local kv head;
+    // resident heads (Alg. 1 line 8 "Update GPU KV cache") append on the compute stream instead
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
     const size_t row_bytes = static_cast<size_t>(d) * 2;
     for (int h = 0; h < Hkv; ++h) {
         const __nv_bfloat16* pk = c->d_pack + (static_cast<size_t>(h) * 2 + 0) * n * d;
         const __nv_bfloat16* pv = c->d_pack + (static_cast<size_t>(h) * 2 + 1) * n * d;
+        if (c->resident(layer, h)) {
+            HI_CK(c, cudaMemcpyAsync(c->dev_k(layer, h, s), pk, n * row_bytes, cudaMemcpyDeviceToDevice, c->s_comp));
+            HI_CK(c, cudaMemcpyAsync(c->dev_v(layer, h, s), pv, n * row_bytes, cudaMemcpyDeviceToDevice, c->s_comp));
+            continue;
+        }
         HI_CK(c, cudaMemcpyAsync(c->host_k(layer, h, s), pk, n * row_bytes, cudaMemcpyDeviceToHost, c->s_d2h));
         HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, s), pv, n * row_bytes, cudaMemcpyDeviceToHost, c->s_d2h));
         c->d2h_bytes += static_cast<int64_t>(2 * n * row_bytes);
@@ -518,13 +561,27 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
         p.kv_row_stride = d;
         p.n_k = n;
         p.k_pos0 = s;
-        p.flags = hi::PF_FIRST | hi::PF_CAUSAL | (nb == 0 ? hi::PF_LAST : 0);
+        p.flags = hi::PF_FIRST | hi::PF_CAUSAL | (s == 0 ? hi::PF_LAST : 0);
         {
             LaunchTimer tm(c);
             HI_CK(c, launch_prefill(c, p));
             tm.done(4.0 * d * g * (static_cast<double>(n) * (n + 1) / 2.0), true);
         }
         ++c->launches;
+        if (c->resident(layer, h)) {  // H_on: the whole history [0, s) straight from the HBM cache
+            if (s > 0) {
+                p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, h, 0));
+                p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, h, 0));
+                p.n_k = static_cast<int>(s);
+                p.k_pos0 = 0;
+                p.flags = hi::PF_LAST;
+                LaunchTimer tm(c);
+                HI_CK(c, launch_prefill(c, p));
+                tm.done(4.0 * d * g * static_cast<double>(n) * static_cast<double>(s), true);
+                ++c->launches;
+            }
+            continue;
+        }
         // history blocks [0, s) through the staging slots (Alg. 1 line 10 prefetch)
         for (int64_t b = 0; b < nb; ++b) {
             const int64_t k0 = b * c->slot_tokens;
@@ -577,6 +634,13 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     // append (Alg. 1 line 26 "Async Update CPU KV cache"): host row s of every local kv head
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
     for (int h = 0; h < Hkv; ++h) {
+        if (c->resident(layer, h)) {  // H_on: append in HBM (compute stream; read by later calls only)
+            HI_CK(c, cudaMemcpyAsync(c->dev_k(layer, h, s), kn + static_cast<size_t>(h) * d, row_bytes,
+                                     cudaMemcpyDeviceToDevice, c->s_comp));
+            HI_CK(c, cudaMemcpyAsync(c->dev_v(layer, h, s), vn + static_cast<size_t>(h) * d, row_bytes,
+                                     cudaMemcpyDeviceToDevice, c->s_comp));
+            continue;
+        }
         HI_CK(c, cudaMemcpyAsync(c->host_k(layer, h, s), kn + static_cast<size_t>(h) * d, row_bytes,
                                  cudaMemcpyDeviceToHost, c->s_d2h));
         HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, s), vn + static_cast<size_t>(h) * d, row_bytes,
@@ -588,9 +652,28 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
 
     // history: per kv head, blocks through the slots -> split-K partial records
     const int64_t nb = (s + c->slot_tokens - 1) / c->slot_tokens;
-    int n_parts = 0;
+    int n_parts_off = 0, n_parts_res = 0;
     for (int h = 0; h < Hkv; ++h) {
         int pofs = 0;
+        if (c->resident(layer, h)) {  // H_on: one split-K pass over [0, s) in HBM
+            if (s > 0) {
+                hi::DecodePartialParams p{};
+                p.q = static_cast<const __nv_bfloat16*>(q) + static_cast<size_t>(h) * g * d;
+                p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, h, 0));
+                p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, h, 0));
+                p.n_k = static_cast<int>(s);
+                p.split_len = decode_split_len(s);
+                p.scale_log2 = c->scale_log2;
+                p.parts = c->d_parts + static_cast<size_t>(h) * c->max_parts * g * (d + 4);
+                pofs = static_cast<int>((s + p.split_len - 1) / p.split_len);
+                LaunchTimer tm(c);
+                HI_CK(c, hi::launch_decode_partial(p, d, g, pofs, c->s_comp));
+                tm.done(4.0 * d * static_cast<double>(s), false);
+                ++c->launches;
+            }
+            n_parts_res = pofs;
+            continue;
+        }
         for (int64_t b = 0; b < nb; ++b) {
             const int64_t k0 = b * c->slot_tokens;
             const int64_t nk = std::min<int64_t>(c->slot_tokens, s - k0);
@@ -616,7 +699,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
             st = release_slot(c, slot);
             if (st != HI_OK) return st;
         }
-        n_parts = pofs;
+        n_parts_off = pofs;
     }
     hi::DecodeCombineParams cp{};
     cp.q = static_cast<const __nv_bfloat16*>(q);
@@ -624,7 +707,9 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     cp.v_new = vn;
     cp.parts = c->d_parts;
     cp.max_parts = c->max_parts;
-    cp.n_parts = n_parts;
+    cp.n_parts = n_parts_off;
+    cp.n_parts_lo = n_parts_res;
+    cp.h_lo = c->resident_heads_of_layer(layer);
     cp.g = g;
     cp.scale_log2 = c->scale_log2;
     cp.out = static_cast<__nv_bfloat16*>(out);
@@ -652,6 +737,13 @@ hi_status hi_read_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, v
     if (st != HI_OK) return st;
     if (h < 0 || h >= c->Hkv_loc || pos < 0 || n < 0 || pos + n > c->max_ctx || (n > 0 && (!k_dst || !v_dst)))
         return set_err(c, HI_ESHAPE, "bad host KV range");
+    if (c->resident(layer, h)) {
+        st = hi_synchronize(c);
+        if (st != HI_OK) return st;
+        HI_CK(c, cudaMemcpy(k_dst, c->dev_k(layer, h, pos), static_cast<size_t>(n) * c->d * 2, cudaMemcpyDeviceToHost));
+        HI_CK(c, cudaMemcpy(v_dst, c->dev_v(layer, h, pos), static_cast<size_t>(n) * c->d * 2, cudaMemcpyDeviceToHost));
+        return HI_OK;
+    }
     HI_CK(c, cudaStreamSynchronize(c->s_d2h));
     memcpy(k_dst, c->host_k(layer, h, pos), static_cast<size_t>(n) * c->d * 2);
     memcpy(v_dst, c->host_v(layer, h, pos), static_cast<size_t>(n) * c->d * 2);
@@ -667,6 +759,12 @@ hi_status hi_write_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, 
     st = hi_synchronize(c);
     if (st != HI_OK) return st;
     const size_t bytes = static_cast<size_t>(n) * c->d * 2;
+    if (c->resident(layer, h)) {
+        const cudaMemcpyKind kind = from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        HI_CK(c, cudaMemcpy(c->dev_k(layer, h, pos), k_src, bytes, kind));
+        HI_CK(c, cudaMemcpy(c->dev_v(layer, h, pos), v_src, bytes, kind));
+        return HI_OK;
+    }
     if (from_device) {
         HI_CK(c, cudaMemcpyAsync(c->host_k(layer, h, pos), k_src, bytes, cudaMemcpyDeviceToHost, c->s_d2h));
         HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, pos), v_src, bytes, cudaMemcpyDeviceToHost, c->s_d2h));
@@ -716,6 +814,8 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     o->decode_attn_bytes = c->decode_bytes;
     o->decode_attn_launches = c->decode_timed;
     o->init_seconds = c->init_seconds;
+    o->resident_kv_heads = c->n_res;
+    o->resident_bytes = static_cast<int64_t>(c->res_bytes);
     o->numa_node = c->numa_node;
     o->n_slots = c->n_slots;
     o->slot_tokens = c->slot_tokens;

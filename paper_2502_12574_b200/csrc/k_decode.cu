@@ -15,8 +15,6 @@
 namespace hi {
 namespace {
 
-constexpr int DEC_THREADS = 128;
-constexpr int DEC_UNROLL = 4;
 
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
@@ -33,23 +31,95 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
     }
 }
 
-__device__ __forceinline__ uint4 ld_stream(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    return r;
+
+// ---- PTX helpers: mbarrier + bulk async copy (TMA engine, non-tensor form) --------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (uint32_t it = 0;; ++it) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+        if (done) return;
+        if (it > (1u << 31)) __trap();
+    }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
 }
 
-// One CTA = keys [blockIdx.x*split_len, +split_len) of the block.  Lane layout: LPK = D/8 lanes
-// hold one key row (16 B each); KPW = 32/LPK keys per warp step.
+constexpr int TD_CONSUMERS = 8;                       // consumer warps
+constexpr int TD_THREADS = (TD_CONSUMERS + 1) * 32;   // + 1 producer warp
+constexpr int TD_STAGES = 4;
+template <int G>
+constexpr int td_chunk() { return G >= 8 ? 32 : 64; }  // keys per pipeline stage (register budget at g = 8)
+
 template <int D, int G>
-__global__ void __launch_bounds__(DEC_THREADS) decode_partial_kernel(const DecodePartialParams p) {
+constexpr int td_smem_bytes() { return TD_STAGES * 2 * td_chunk<G>() * D * 2 + 2 * TD_STAGES * 8 + 128; }
+
+// One CTA = keys [blockIdx.x*split_len, +split_len) of the block.  One producer thread streams the
+// CTA's contiguous K and V rows into a TD_STAGES-deep shared-memory ring with cp.async.bulk (the
+// TMA engine: a few bulk requests keep >100 KiB in flight per SM, which is what HBM latency needs);
+// 8 consumer warps compute from shared memory.  Lane layout: LPK = D/8 lanes hold one key row
+// (16 B each); KPW = 32/LPK keys per warp step.
+template <int D, int G>
+__global__ void __launch_bounds__(TD_THREADS, 1) decode_partial_kernel(const DecodePartialParams p) {
     constexpr int LPK = D / 8;
     constexpr int KPW = 32 / LPK;
-    constexpr int NW = DEC_THREADS / 32;
+    constexpr int NW = TD_CONSUMERS;
+    constexpr int TD_CHUNK = td_chunk<G>();
+    constexpr int STAGE_BYTES = 2 * TD_CHUNK * D * 2;
+    extern __shared__ __align__(128) uint8_t td_smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(td_smem + TD_STAGES * STAGE_BYTES);
+    const uint32_t sbase = smem_u32(td_smem);
+    auto bar_full = [&](int s) { return smem_u32(&bars[s]); };
+    auto bar_empty = [&](int s) { return smem_u32(&bars[TD_STAGES + s]); };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sub = lane / LPK, part = lane % LPK;
 
+    const int k_begin = blockIdx.x * p.split_len;
+    const int k_end = min(p.n_k, k_begin + p.split_len);
+    const int n_chunks = (k_end - k_begin + TD_CHUNK - 1) / TD_CHUNK;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TD_STAGES; ++s) {
+            mbar_init(bar_full(s), 1);
+            mbar_init(bar_empty(s), NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // ---------------- producer: bulk copies of K and V rows into the ring ----------------
+        if (lane == 0) {
+            for (int i = 0; i < n_chunks; ++i) {
+                const int s = i % TD_STAGES;
+                if (i >= TD_STAGES) mbar_wait(bar_empty(s), ((i / TD_STAGES) - 1) & 1);
+                const int k0 = k_begin + i * TD_CHUNK;
+                const uint32_t bytes = static_cast<uint32_t>(min(TD_CHUNK, k_end - k0)) * D * 2;
+                mbar_expect_tx(bar_full(s), 2 * bytes);
+                bulk_g2s(sbase + s * STAGE_BYTES, p.k + static_cast<int64_t>(k0) * D, bytes, bar_full(s));
+                bulk_g2s(sbase + s * STAGE_BYTES + TD_CHUNK * D * 2, p.v + static_cast<int64_t>(k0) * D, bytes,
+                         bar_full(s));
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    const int sub = lane / LPK, part = lane % LPK;
     float q[G][8];
 #pragma unroll
     for (int j = 0; j < G; ++j) {
@@ -66,60 +136,65 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_partial_kernel(const Decod
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[j][i] = 0.f;
     }
-
-    const int k_begin = blockIdx.x * p.split_len;
-    const int k_end = min(p.n_k, k_begin + p.split_len);
-    // warp w handles keys k_begin + (step*NW + w)*KPW + sub
-    for (int base = k_begin + warp * KPW; base < k_end; base += NW * KPW * DEC_UNROLL) {
-        uint4 kr[DEC_UNROLL], vr[DEC_UNROLL];
-        bool valid[DEC_UNROLL];
+    constexpr int KEYS_PER_WARP = TD_CHUNK / NW;
+    constexpr int U = KEYS_PER_WARP / KPW;                 // key steps per warp per chunk
+    for (int i = 0; i < n_chunks; ++i) {
+        const int s = i % TD_STAGES;
+        mbar_wait(bar_full(s), (i / TD_STAGES) & 1);
+        const int nk = min(TD_CHUNK, k_end - (k_begin + i * TD_CHUNK));
+        const uint8_t* sk = td_smem + s * STAGE_BYTES;
+        const uint8_t* sv = sk + TD_CHUNK * D * 2;
+        uint4 kr[U], vr[U];
+        bool valid[U];
 #pragma unroll
-        for (int u = 0; u < DEC_UNROLL; ++u) {
-            const int key = base + u * NW * KPW + sub;
-            valid[u] = key < k_end;
-            const int64_t off = static_cast<int64_t>(valid[u] ? key : k_begin) * D + part * 8;
-            kr[u] = ld_stream(p.k + off);
-            vr[u] = ld_stream(p.v + off);
+        for (int u = 0; u < U; ++u) {
+            const int key = warp * KEYS_PER_WARP + u * KPW + sub;
+            valid[u] = key < nk;
+            const int kk = valid[u] ? key : 0;
+            kr[u] = *reinterpret_cast<const uint4*>(sk + kk * D * 2 + part * 16);
+            vr[u] = *reinterpret_cast<const uint4*>(sv + kk * D * 2 + part * 16);
         }
-        float x[DEC_UNROLL][G];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty(s));  // this warp's reads of stage s are done
+        float x[U][G];
 #pragma unroll
-        for (int u = 0; u < DEC_UNROLL; ++u) {
+        for (int u = 0; u < U; ++u) {
             float kf[8];
             bf16x8_to_f32(kr[u], kf);
 #pragma unroll
             for (int j = 0; j < G; ++j) {
                 float acc = 0.f;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) acc = fmaf(q[j][i], kf[i], acc);
+                for (int e = 0; e < 8; ++e) acc = fmaf(q[j][e], kf[e], acc);
                 x[u][j] = acc;
             }
         }
 #pragma unroll
         for (int off = 1; off < LPK; off <<= 1)
 #pragma unroll
-            for (int u = 0; u < DEC_UNROLL; ++u)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
                 for (int j = 0; j < G; ++j) x[u][j] += __shfl_xor_sync(0xffffffffu, x[u][j], off);
 #pragma unroll
         for (int j = 0; j < G; ++j) {
             float mx = m[j];
 #pragma unroll
-            for (int u = 0; u < DEC_UNROLL; ++u)
+            for (int u = 0; u < U; ++u)
                 if (valid[u]) mx = fmaxf(mx, x[u][j]);
             const float alpha = (m[j] == -CUDART_INF_F) ? 0.f : fast_exp2(m[j] - mx);
             m[j] = mx;
             l[j] *= alpha;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) o[j][i] *= alpha;
+            for (int e = 0; e < 8; ++e) o[j][e] *= alpha;
 #pragma unroll
-            for (int u = 0; u < DEC_UNROLL; ++u) {
+            for (int u = 0; u < U; ++u) {
                 if (!valid[u]) continue;
                 const float pw = fast_exp2(x[u][j] - mx);
                 l[j] += pw;
                 float vf[8];
                 bf16x8_to_f32(vr[u], vf);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) o[j][i] = fmaf(pw, vf[i], o[j][i]);
+                for (int e = 0; e < 8; ++e) o[j][e] = fmaf(pw, vf[e], o[j][e]);
             }
         }
     }
@@ -136,37 +211,40 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_partial_kernel(const Decod
             const float a2 = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - mx);
             l[j] = l[j] * a1 + l2 * a2;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float o2 = __shfl_xor_sync(0xffffffffu, o[j][i], off);
-                o[j][i] = o[j][i] * a1 + o2 * a2;
+            for (int e = 0; e < 8; ++e) {
+                const float o2 = __shfl_xor_sync(0xffffffffu, o[j][e], off);
+                o[j][e] = o[j][e] * a1 + o2 * a2;
             }
             m[j] = mx;
         }
     }
-    // merge the warps through shared memory
-    __shared__ float sm_m[NW][G], sm_l[NW][G];
-    __shared__ float sm_o[NW][G][D];
+    // merge the consumer warps through shared memory (the ring is free: every chunk was consumed)
+    float* sm_m = reinterpret_cast<float*>(td_smem);          // [NW][G]
+    float* sm_l = sm_m + NW * G;                              // [NW][G]
+    float* sm_o = sm_l + NW * G;                              // [NW][G][D]
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // all consumers done with the ring
     if (sub == 0) {
 #pragma unroll
         for (int j = 0; j < G; ++j) {
-            if (part == 0) { sm_m[warp][j] = m[j]; sm_l[warp][j] = l[j]; }
+            if (part == 0) { sm_m[warp * G + j] = m[j]; sm_l[warp * G + j] = l[j]; }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) sm_o[warp][j][part * 8 + i] = o[j][i];
+            for (int e = 0; e < 8; ++e) sm_o[(warp * G + j) * D + part * 8 + e] = o[j][e];
         }
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
     float* rec = p.parts + static_cast<int64_t>(blockIdx.x) * G * (D + 4);
-    for (int idx = threadIdx.x; idx < G * D; idx += DEC_THREADS) {
+    for (int idx = threadIdx.x; idx < G * D; idx += NW * 32) {
         const int j = idx / D, c = idx % D;
         float mx = -CUDART_INF_F;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) mx = fmaxf(mx, sm_m[w][j]);
+        for (int w = 0; w < NW; ++w) mx = fmaxf(mx, sm_m[w * G + j]);
         float lsum = 0.f, osum = 0.f;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            const float a = (sm_m[w][j] == -CUDART_INF_F) ? 0.f : fast_exp2(sm_m[w][j] - mx);
-            lsum += a * sm_l[w][j];
-            osum += a * sm_o[w][j][c];
+            const float mw = sm_m[w * G + j];
+            const float a = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - mx);
+            lsum += a * sm_l[w * G + j];
+            osum += a * sm_o[(w * G + j) * D + c];
         }
         float* r = rec + j * (D + 4);
         r[4 + c] = osum;
@@ -201,11 +279,12 @@ __global__ void __launch_bounds__(D) decode_combine_kernel(const DecodeCombinePa
     const float* recs = p.parts + (static_cast<int64_t>(h) * p.max_parts * p.g + j) * (D + 4);
     const int64_t rstride = static_cast<int64_t>(p.g) * (D + 4);
     float mx = x;
-    for (int i = 0; i < p.n_parts; ++i) mx = fmaxf(mx, recs[i * rstride]);
+    const int n_parts = h < p.h_lo ? p.n_parts_lo : p.n_parts;
+    for (int i = 0; i < n_parts; ++i) mx = fmaxf(mx, recs[i * rstride]);
     const float a0 = fast_exp2(x - mx);
     float lsum = a0;
     float osum = a0 * __bfloat162float(p.v_new[h * D + c]);
-    for (int i = 0; i < p.n_parts; ++i) {
+    for (int i = 0; i < n_parts; ++i) {
         const float* r = recs + i * rstride;
         const float mi = r[0];
         const float a = (mi == -CUDART_INF_F) ? 0.f : fast_exp2(mi - mx);
@@ -217,7 +296,14 @@ __global__ void __launch_bounds__(D) decode_combine_kernel(const DecodeCombinePa
 
 template <int D, int G>
 cudaError_t launch_partial_dg(const DecodePartialParams& p, int n_splits, cudaStream_t s) {
-    decode_partial_kernel<D, G><<<n_splits, DEC_THREADS, 0, s>>>(p);
+    constexpr int smem = td_smem_bytes<D, G>();
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(decode_partial_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    decode_partial_kernel<D, G><<<n_splits, TD_THREADS, smem, s>>>(p);
     return cudaGetLastError();
 }
 template <int D>

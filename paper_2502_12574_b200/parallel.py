@@ -30,6 +30,13 @@ def gather_heads(out_local: torch.Tensor, group=None, out: torch.Tensor | None =
     world = dist.get_world_size(group)
     if out is None:
         out = torch.empty((world, *out_local.shape), dtype=out_local.dtype, device=out_local.device)
+    if out_local.is_cuda and dist.get_backend(group) == "gloo":
+        # validation mode (several ranks sharing one GPU, e.g. bench.py --ranks-share-gpu): gloo has no
+        # CUDA all-gather, so stage through host memory.  The NCCL path below is the product path.
+        parts = [torch.empty(out_local.shape, dtype=out_local.dtype) for _ in range(world)]
+        dist.all_gather(parts, out_local.cpu(), group=group)
+        out.copy_(torch.stack(parts))
+        return out
     dist.all_gather_into_tensor(out.view(-1), out_local.contiguous().view(-1), group=group)
     return out
 

@@ -1,0 +1,74 @@
+"""Full-size parity: the Llama-3-8B head geometry at the 128K context of BASELINE.json configs[1],
+in bench.py's launch configuration (chunk 18944, 4 staging slots of max_ctx/4 tokens), on sampled
+rows the oracle computes one by one, plus a bit-exact host-KV scan.  Layers are reduced to 2 (every
+layer call runs the identical launch sequence)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from conftest import cuda_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a GPU")]
+
+SEED = synth.BASE_SEED
+
+
+def _gen(tensor, dist, layer, head0, nh, pos0, n, d):
+    from synth.cuda import gen_block_cuda
+    return gen_block_cuda(SEED, tensor, dist, layer, head0, nh, pos0, n, d)
+
+
+@pytest.mark.parametrize("dist", ["U", "P"])
+def test_llama8b_128k_sampled_rows_and_host_kv(dist):
+    from oracle import attention_rows
+    from paper_2502_12574_b200.headinfer import HeadInfer
+    L, hq, hkv, d, S, c, n_dec = 2, 32, 8, 128, 131072, 18944, 3
+    g = hq // hkv
+    hi = HeadInfer(L, hq, hkv, d, S + n_dec, c)
+    sample = {}  # (layer) -> list of (pos, out row [hq, d])
+    rng = np.random.default_rng(0)
+    chunk_starts = list(range(0, S, c))
+    want = set()
+    for s0 in chunk_starts:  # first/last row of every chunk, plus random rows
+        want.update([s0, min(S, s0 + c) - 1])
+    want.update(rng.integers(0, S, 24).tolist())
+    for s0 in chunk_starts:
+        n = min(c, S - s0)
+        for layer in range(L):
+            Q, K, V = (_gen(t, dist, layer, 0, h, s0, n, d) for t, h in ((0, hq), (1, hkv), (2, hkv)))
+            out = hi.prefill_chunk(layer, Q, K, V)
+            rows = [p for p in want if s0 <= p < s0 + n]
+            if rows:
+                o = out[torch.tensor([p - s0 for p in rows], device="cuda")].float().cpu().numpy()
+                for p, r in zip(rows, o):
+                    sample.setdefault(layer, []).append((p, r))
+    for t in range(n_dec):
+        p = S + t
+        for layer in range(L):
+            q, k, v = (_gen(tt, dist, layer, 0, h, p, 1, d)[0] for tt, h in ((0, hq), (1, hkv), (2, hkv)))
+            o = hi.decode(layer, q, k, v).float().cpu().numpy()
+            sample.setdefault(layer, []).append((p, o))
+    hi.synchronize()
+    maxerr, sumerr, cnt = 0.0, 0.0, 0
+    for layer in range(L):
+        pos = np.array([p for p, _ in sample[layer]])
+        got = np.stack([r for _, r in sample[layer]])  # [R, hq, d]
+        qpos = np.concatenate([synth.gen_block(SEED, 0, dist, layer, 0, hq, int(p), 1, d) for p in pos])  # [R, hq, d]
+        for h in range(hkv):
+            k = _gen(1, dist, layer, h, 1, 0, S + n_dec, d)[:, 0].cpu().view(torch.int16).numpy().view(np.uint16)
+            v = _gen(2, dist, layer, h, 1, 0, S + n_dec, d)[:, 0].cpu().view(torch.int16).numpy().view(np.uint16)
+            # host KV store must hold exactly these bytes
+            hk, hv = hi.read_host_kv(layer, h, 0, S + n_dec)
+            assert np.array_equal(hk.view(torch.int16).numpy().view(np.uint16), k), (layer, h)
+            assert np.array_equal(hv.view(torch.int16).numpy().view(np.uint16), v), (layer, h)
+            for j in range(h * g, (h + 1) * g):
+                ref = attention_rows(qpos[:, j], pos, k, v)
+                err = np.abs(got[:, j] - ref)
+                maxerr = max(maxerr, float(err.max()))
+                sumerr += float(err.sum())
+                cnt += err.size
+    st = hi.stats()
+    hi.close()
+    assert maxerr <= 2e-2 and sumerr / cnt <= 2e-3, (maxerr, sumerr / cnt)
+    assert st["staging_bytes"] <= st["staging_bound_bytes"]

@@ -144,3 +144,20 @@ def test_gpu_generator_matches_cpu_bits():
             a = gen_block_cuda(99, t, dist, 3, 1, 5, 0, 300, 128).cpu().view(torch.int16).numpy().view(np.uint16)
             b = synth.gen_block(99, t, dist, 3, 1, 5, 0, 300, 128)
             assert np.array_equal(a, b), (dist, t)
+
+
+@pytest.mark.parametrize("resident", [1, 3, 8, -1])
+def test_resident_heads_next1(resident):
+    """NEXT-1 (Alg. 1 H_on branch): the first R (layer, kv head) pairs keep their KV in HBM; results and
+    the KV store contents must not depend on R (R = -1: as many as fit)."""
+    r = Run(layers=2, q_heads=8, kv_heads=4, d=128, chunks=[300, 300, 100], n_decode=4, dist="P",
+            opts=dict(slot_tokens=128, resident_kv_heads=resident))
+    gpu, ctx = run_gpu(r)
+    ref, inputs = run_oracle(r)
+    compare(gpu, ref)
+    check_host_kv(ctx, r, inputs)
+    st = ctx.stats()
+    assert st["resident_kv_heads"] == (8 if resident == -1 else resident)
+    if st["resident_kv_heads"] == 8:
+        assert st["host_store_bytes"] == 0 and st["h2d_bytes"] == 0
+    ctx.close()
