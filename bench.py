@@ -330,11 +330,12 @@ def run_ours(args, rank, world, local_rank, pg):
     dk_ms = sd1["decode_attn_ms"] - sd0["decode_attn_ms"]
     # step rooflines (measured peaks; sustained tensor peak inside a long step)
     pk = dict(peaks, bf16_tflops=peak_t)
-    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, last_chunk_pos - c * (K - 1) // 2, c, world), pk)
-    t_roof_pre = sum(rf.step_roofline_seconds(rf.prefill_step(shape, s0 + (W + i) * c, c, world), pk)["seconds"]
+    R = st1["resident_kv_heads"]
+    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, last_chunk_pos - c * (K - 1) // 2, c, world, R), pk)
+    t_roof_pre = sum(rf.step_roofline_seconds(rf.prefill_step(shape, s0 + (W + i) * c, c, world, R), pk)["seconds"]
                      for i in range(K))
-    t_roof_dec = sum(rf.step_roofline_seconds(rf.decode_step(shape, S + i, world), pk)["seconds"]
-                     for i in range(W, W + K))
+    dec_roofs = [rf.step_roofline_seconds(rf.decode_step(shape, S + i, world, R), pk) for i in range(W, W + K)]
+    t_roof_dec = sum(x["seconds"] for x in dec_roofs)
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "ncu_prefill_traffic.json")
     if os.path.exists(prof_path):
@@ -365,7 +366,7 @@ def run_ours(args, rank, world, local_rank, pg):
                    "l2": "inputs per step > L2 (>= 6 GiB), no flush needed"},
         "decode": {"ms_per_token": round(dec_ms_tok, 3), "h2d_gbs": round(h2d_gbs, 2),
                    "link_peak_gbs": peaks["h2d_gbs"], "link_frac": round(h2d_gbs / peaks["h2d_gbs"], 4),
-                   "roofline_frac": round(t_roof_dec / (dec_ms / 1e3), 4),
+                   "roofline_frac": round(t_roof_dec / (dec_ms / 1e3), 4), "roofline_bound": dec_roofs[-1]["bound"],
                    "h2d_bytes_per_token": int(h2d_dec),
                    "kernel": {"bound": "hbm", "achieved_gbs": round(dk_bytes / (dk_ms / 1e3) / 1e9, 1) if dk_ms else None,
                               "peak_gbs": peaks["hbm_gbs"],

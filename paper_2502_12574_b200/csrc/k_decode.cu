@@ -252,46 +252,78 @@ __global__ void __launch_bounds__(TD_THREADS, 1) decode_partial_kernel(const Dec
     }
 }
 
-// One CTA per local q head: merge the n_parts records of its kv head with the new key.
+// One CTA (8 warps) per local q head: merge the n_parts records of its kv head with the new key.
+// Pass 1: block max over the record maxima (and the new key's score); pass 2: each warp accumulates
+// a strided subset of records (lane = D/32 consecutive columns, float4/float2 loads, 4 records in
+// flight), then the warps are merged in shared memory.
+constexpr int CB_WARPS = 8;
+
 template <int D>
-__global__ void __launch_bounds__(D) decode_combine_kernel(const DecodeCombineParams p) {
-    const int jq = blockIdx.x;          // local q head
+__global__ void __launch_bounds__(CB_WARPS * 32) decode_combine_kernel(const DecodeCombineParams p) {
+    constexpr int CPL = D / 32;  // columns per lane
+    const int jq = blockIdx.x;   // local q head
     const int h = jq / p.g, j = jq % p.g;
-    const int c = threadIdx.x;
-    __shared__ float red[D / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ float s_red[CB_WARPS];
     __shared__ float s_x;
-    // score of the new key (the token attends itself, reading R3)
-    const float qc = __bfloat162float(p.q[jq * D + c]);
-    const float kc = __bfloat162float(p.k_new[h * D + c]);
-    float prod = qc * kc;
+    __shared__ float s_o[CB_WARPS][D];
+    __shared__ float s_l[CB_WARPS];
+    // score of the new key (the token attends itself, reading R3): warp 0
+    if (warp == 0) {
+        float prod = 0.f;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, off);
-    if ((c & 31) == 0) red[c >> 5] = prod;
-    __syncthreads();
-    if (c == 0) {
-        float t = 0.f;
+        for (int c = 0; c < CPL; ++c) {
+            const int col = lane * CPL + c;
+            prod += __bfloat162float(p.q[jq * D + col]) * __bfloat162float(p.k_new[h * D + col]);
+        }
 #pragma unroll
-        for (int w = 0; w < D / 32; ++w) t += red[w];
-        s_x = t * p.scale_log2;
+        for (int off = 16; off > 0; off >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, off);
+        if (lane == 0) s_x = prod * p.scale_log2;
     }
-    __syncthreads();
-    const float x = s_x;
+    const int n_parts = h < p.h_lo ? p.n_parts_lo : p.n_parts;
     const float* recs = p.parts + (static_cast<int64_t>(h) * p.max_parts * p.g + j) * (D + 4);
     const int64_t rstride = static_cast<int64_t>(p.g) * (D + 4);
-    float mx = x;
-    const int n_parts = h < p.h_lo ? p.n_parts_lo : p.n_parts;
-    for (int i = 0; i < n_parts; ++i) mx = fmaxf(mx, recs[i * rstride]);
-    const float a0 = fast_exp2(x - mx);
-    float lsum = a0;
-    float osum = a0 * __bfloat162float(p.v_new[h * D + c]);
-    for (int i = 0; i < n_parts; ++i) {
+    float mx = -CUDART_INF_F;
+    for (int i = threadIdx.x; i < n_parts; i += CB_WARPS * 32) mx = fmaxf(mx, recs[i * rstride]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (lane == 0) s_red[warp] = mx;
+    __syncthreads();
+    float M = s_x;
+#pragma unroll
+    for (int w = 0; w < CB_WARPS; ++w) M = fmaxf(M, s_red[w]);
+    float o[CPL], lsum = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) o[c] = 0.f;
+#pragma unroll 4
+    for (int i = warp; i < n_parts; i += CB_WARPS) {
         const float* r = recs + i * rstride;
         const float mi = r[0];
-        const float a = (mi == -CUDART_INF_F) ? 0.f : fast_exp2(mi - mx);
+        const float a = (mi == -CUDART_INF_F) ? 0.f : fast_exp2(mi - M);
         lsum += a * r[1];
-        osum += a * r[4 + c];
+        if constexpr (CPL == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(r + 4 + lane * 4);
+            o[0] += a * v.x; o[1] += a * v.y; o[2] += a * v.z; o[3] += a * v.w;
+        } else {
+            const float2 v = *reinterpret_cast<const float2*>(r + 4 + lane * 2);
+            o[0] += a * v.x; o[1] += a * v.y;
+        }
     }
-    p.out[jq * D + c] = __float2bfloat16_rn(osum / lsum);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) s_o[warp][lane * CPL + c] = o[c];
+    if (lane == 0) s_l[warp] = lsum;
+    __syncthreads();
+    if (threadIdx.x < D) {
+        const int c = threadIdx.x;
+        const float a0 = fast_exp2(s_x - M);
+        float L = a0, O = a0 * __bfloat162float(p.v_new[h * D + c]);
+#pragma unroll
+        for (int w = 0; w < CB_WARPS; ++w) {
+            L += s_l[w];
+            O += s_o[w][c];
+        }
+        p.out[jq * D + c] = __float2bfloat16_rn(O / L);
+    }
 }
 
 template <int D, int G>
@@ -327,8 +359,8 @@ cudaError_t launch_decode_partial(const DecodePartialParams& p, int d, int g, in
 }
 
 cudaError_t launch_decode_combine(const DecodeCombineParams& p, int d, int hq_loc, cudaStream_t stream) {
-    if (d == 64) decode_combine_kernel<64><<<hq_loc, 64, 0, stream>>>(p);
-    else if (d == 128) decode_combine_kernel<128><<<hq_loc, 128, 0, stream>>>(p);
+    if (d == 64) decode_combine_kernel<64><<<hq_loc, CB_WARPS * 32, 0, stream>>>(p);
+    else if (d == 128) decode_combine_kernel<128><<<hq_loc, CB_WARPS * 32, 0, stream>>>(p);
     else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }

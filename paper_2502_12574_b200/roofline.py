@@ -50,26 +50,30 @@ def kv_bytes(d: int, tokens: int) -> int:
     return 4 * d * tokens
 
 
-def prefill_step(shape: Shape, s: int, n: int, world: int = 1) -> dict:
-    """One prefill chunk over all layers on one rank (H_kv/world local heads)."""
-    hkv = shape.kv_heads // world
-    d, g, L = shape.head_dim, shape.g, shape.layers
+def prefill_step(shape: Shape, s: int, n: int, world: int = 1, resident: int = 0) -> dict:
+    """One prefill chunk over all layers on one rank (H_kv/world local heads); `resident` of the
+    rank's (layer, kv head) pairs keep their KV in HBM (NEXT-1): no link traffic, one HBM read."""
+    pairs = shape.layers * (shape.kv_heads // world)
+    off = pairs - resident
+    d, g = shape.head_dim, shape.g
     return {
-        "flops": L * hkv * prefill_flops(d, g, s, n),
-        "h2d_bytes": L * hkv * kv_bytes(d, s),
-        "d2h_bytes": L * hkv * kv_bytes(d, n),
-        "hbm_bytes": L * hkv * (2 * kv_bytes(d, s) + kv_bytes(d, n) + 4 * d * g * n),
+        "flops": pairs * prefill_flops(d, g, s, n),
+        "h2d_bytes": off * kv_bytes(d, s),
+        "d2h_bytes": off * kv_bytes(d, n),
+        "hbm_bytes": off * 2 * kv_bytes(d, s) + resident * kv_bytes(d, s)
+        + pairs * (kv_bytes(d, n) + 4 * d * g * n),
     }
 
 
-def decode_step(shape: Shape, s: int, world: int = 1) -> dict:
-    hkv = shape.kv_heads // world
-    d, g, L = shape.head_dim, shape.g, shape.layers
+def decode_step(shape: Shape, s: int, world: int = 1, resident: int = 0) -> dict:
+    pairs = shape.layers * (shape.kv_heads // world)
+    off = pairs - resident
+    d, g = shape.head_dim, shape.g
     return {
-        "flops": L * hkv * decode_flops(d, g, s),
-        "h2d_bytes": L * hkv * kv_bytes(d, s),
-        "d2h_bytes": L * hkv * kv_bytes(d, 1),
-        "hbm_bytes": L * hkv * 2 * kv_bytes(d, s),
+        "flops": pairs * decode_flops(d, g, s),
+        "h2d_bytes": off * kv_bytes(d, s),
+        "d2h_bytes": off * kv_bytes(d, 1),
+        "hbm_bytes": off * 2 * kv_bytes(d, s) + resident * kv_bytes(d, s),
     }
 
 
