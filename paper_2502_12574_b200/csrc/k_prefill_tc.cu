@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, b, ID_O,
                                  (j > 0 || kk > 0 || !first) ? 1u : 0u);
                 }
-                umma_commit(bar_o(tt));
+                if (j + 1 == nk_t[tt]) umma_commit(bar_o(tt));  // O final: the epilogue's only wait
             };
             mbar_wait(bar_k(0), 0);
             tc_fence_after();
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             // ---- epilogue ----
             if (nkt > 0) {
-                mbar_wait(bar_o(tt), (nkt - 1) & 1);
+                mbar_wait(bar_o(tt), 0);
                 tc_fence_after();
             }
             if (last) {
