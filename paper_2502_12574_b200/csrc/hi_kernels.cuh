@@ -1,11 +1,17 @@
 // hi_kernels.cuh -- internal launch interface between the host runtime (hi_runtime.cu)
 // and the device kernels of libheadinfer.so.  Not part of the public ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace hi {
+
+// TMA tensor map over a bf16 tensor, SWIZZLE_128B, (tmap.cu); dims/strides innermost-first, strides in
+// bytes (rank-1 entries).  false if the driver entry point is unavailable or the encode fails.
+bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
+                    const cuuint32_t* box);
 
 // ---- prefill attention over one KV segment -------------------------
 // Computes, for the g q heads of one kv head group, rows r = t*g + j (token t of the chunk,

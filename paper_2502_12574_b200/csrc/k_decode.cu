@@ -61,186 +61,198 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  : "memory");
 }
 
-constexpr int TD_CONSUMERS = 8;                       // consumer warps
-constexpr int TD_THREADS = (TD_CONSUMERS + 1) * 32;   // + 1 producer warp
-constexpr int TD_STAGES = 4;
-template <int G>
-constexpr int td_chunk() { return G >= 8 ? 32 : 64; }  // keys per pipeline stage (register budget at g = 8)
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
 
-template <int D, int G>
-constexpr int td_smem_bytes() { return TD_STAGES * 2 * td_chunk<G>() * D * 2 + 2 * TD_STAGES * 8 + 128; }
+constexpr int DM_CONSUMERS = 4;                       // consumer warps, 16 keys each per stage
+constexpr int DM_THREADS = (DM_CONSUMERS + 1) * 32;   // + 1 TMA producer warp
+constexpr int DM_CHUNK = 16 * DM_CONSUMERS;           // keys per pipeline stage
+constexpr int DM_BOX = DM_CHUNK * 128;                // one [64 keys][64 bf16] SW128 box = 8 KiB
+constexpr int DM_STAGES = 6;
+constexpr float DM_RESCALE = 8.0f;                    // lazy O rescale threshold (log2 units)
 
-// One CTA = keys [blockIdx.x*split_len, +split_len) of the block.  One producer thread streams the
-// CTA's contiguous K and V rows into a TD_STAGES-deep shared-memory ring with cp.async.bulk (the
-// TMA engine: a few bulk requests keep >100 KiB in flight per SM, which is what HBM latency needs);
-// 8 consumer warps compute from shared memory.  Lane layout: LPK = D/8 lanes hold one key row
-// (16 B each); KPW = 32/LPK keys per warp step.
+template <int D>
+constexpr int dm_smem_bytes() { return DM_STAGES * 2 * (D / 64) * DM_BOX + 2 * DM_STAGES * 8 + 1024 + 1024; }
+
+// One CTA = keys [blockIdx.x*split_len, +split_len) of the block.  A single producer thread streams
+// the CTA's K and V rows with 2-D TMA (SWIZZLE_128B boxes of 64 keys x 64 dims) into a 6-stage
+// shared-memory ring -- up to 192 KiB in flight per SM, which is what HBM latency needs.  Each of the
+// 4 consumer warps takes 16 keys of a stage and runs them through the tensor cores with warp-level
+// mma.sync m16n8k16: S = Q K^T with the g query rows zero-padded to M = 16 (Q fragments in registers),
+// online softmax on the fp32 accumulators (log2 domain, lazy rescale), O += P V with P re-packed from
+// the S accumulators as the A operand (no shared-memory round trip).  On CUDA cores the same kernel
+// was issue-bound at ~50% of HBM bandwidth (profiles/ncu_decode_r01.txt); with the contraction on the
+// tensor pipe a key costs ~5 warp instructions instead of ~55.
 template <int D, int G>
-__global__ void __launch_bounds__(TD_THREADS, 1) decode_partial_kernel(const DecodePartialParams p) {
-    constexpr int LPK = D / 8;
-    constexpr int KPW = 32 / LPK;
-    constexpr int NW = TD_CONSUMERS;
-    constexpr int TD_CHUNK = td_chunk<G>();
-    constexpr int STAGE_BYTES = 2 * TD_CHUNK * D * 2;
-    extern __shared__ __align__(128) uint8_t td_smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(td_smem + TD_STAGES * STAGE_BYTES);
-    const uint32_t sbase = smem_u32(td_smem);
+__global__ void __launch_bounds__(DM_THREADS, 1)
+    decode_partial_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                          const DecodePartialParams p) {
+    static_assert(G <= 8, "query group must fit the 8 live rows of an m16 tile");
+    constexpr int NB = D / 64;                         // 64-dim boxes per key row
+    constexpr int STAGE = 2 * NB * DM_BOX;
+    extern __shared__ uint8_t dm_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dm_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + DM_STAGES * STAGE);
+    const uint32_t sbase = smem_u32(smem);
     auto bar_full = [&](int s) { return smem_u32(&bars[s]); };
-    auto bar_empty = [&](int s) { return smem_u32(&bars[TD_STAGES + s]); };
+    auto bar_empty = [&](int s) { return smem_u32(&bars[DM_STAGES + s]); };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     const int k_begin = blockIdx.x * p.split_len;
     const int k_end = min(p.n_k, k_begin + p.split_len);
-    const int n_chunks = (k_end - k_begin + TD_CHUNK - 1) / TD_CHUNK;
+    const int n_chunks = (k_end - k_begin + DM_CHUNK - 1) / DM_CHUNK;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TD_STAGES; ++s) {
+        for (int s = 0; s < DM_STAGES; ++s) {
             mbar_init(bar_full(s), 1);
-            mbar_init(bar_empty(s), NW);
+            mbar_init(bar_empty(s), DM_CONSUMERS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == NW) {
-        // ---------------- producer: bulk copies of K and V rows into the ring ----------------
+    if (warp == DM_CONSUMERS) {
+        // ---------------- TMA producer ----------------
         if (lane == 0) {
             for (int i = 0; i < n_chunks; ++i) {
-                const int s = i % TD_STAGES;
-                if (i >= TD_STAGES) mbar_wait(bar_empty(s), ((i / TD_STAGES) - 1) & 1);
-                const int k0 = k_begin + i * TD_CHUNK;
-                const uint32_t bytes = static_cast<uint32_t>(min(TD_CHUNK, k_end - k0)) * D * 2;
-                mbar_expect_tx(bar_full(s), 2 * bytes);
-                bulk_g2s(sbase + s * STAGE_BYTES, p.k + static_cast<int64_t>(k0) * D, bytes, bar_full(s));
-                bulk_g2s(sbase + s * STAGE_BYTES + TD_CHUNK * D * 2, p.v + static_cast<int64_t>(k0) * D, bytes,
-                         bar_full(s));
+                const int s = i % DM_STAGES;
+                if (i >= DM_STAGES) mbar_wait(bar_empty(s), ((i / DM_STAGES) - 1) & 1);
+                const int k0 = k_begin + i * DM_CHUNK;
+                mbar_expect_tx(bar_full(s), STAGE);  // OOB rows of the last chunk are zero-filled, still counted
+#pragma unroll
+                for (int c = 0; c < NB; ++c) {
+                    tma_load_2d(sbase + s * STAGE + c * DM_BOX, &tm_k, bar_full(s), c * 64, k0);
+                    tma_load_2d(sbase + s * STAGE + (NB + c) * DM_BOX, &tm_v, bar_full(s), c * 64, k0);
+                }
             }
         }
         return;
     }
 
     // ---------------- consumers ----------------
-    const int sub = lane / LPK, part = lane % LPK;
-    float q[G][8];
+    const int gid = lane >> 2, tq = lane & 3;
+    const bool row_live = gid < G;
+    // Q fragments (A operand, rows = q heads of the group, zero-padded to 16), all of D
+    uint32_t qa[D / 16][2];  // {a0a1 (row gid, k 0-7 of the step), a4a5 (row gid, k 8-15)}; rows gid+8 are 0
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-        float f[8];
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(p.q + j * D + part * 8), f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) q[j][i] = f[i] * p.scale_log2;  // fold log2(e)/sqrt(d) into q
+    for (int ks = 0; ks < D / 16; ++ks) {
+        qa[ks][0] = row_live ? *reinterpret_cast<const uint32_t*>(p.q + gid * D + ks * 16 + tq * 2) : 0u;
+        qa[ks][1] = row_live ? *reinterpret_cast<const uint32_t*>(p.q + gid * D + ks * 16 + 8 + tq * 2) : 0u;
     }
-    float m[G], l[G], o[G][8];
+    float o[D / 8][4];
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-        m[j] = -CUDART_INF_F;
-        l[j] = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[j][i] = 0.f;
-    }
-    constexpr int KEYS_PER_WARP = TD_CHUNK / NW;
-    constexpr int U = KEYS_PER_WARP / KPW;                 // key steps per warp per chunk
+    for (int nt = 0; nt < D / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+    float m_run = -CUDART_INF_F, l_run = 0.f;  // row gid (l: this thread's partial sum)
+    const float sc = p.scale_log2;
+    const int kb = warp * 16;                 // this warp's 16 keys within a stage
     for (int i = 0; i < n_chunks; ++i) {
-        const int s = i % TD_STAGES;
-        mbar_wait(bar_full(s), (i / TD_STAGES) & 1);
-        const int nk = min(TD_CHUNK, k_end - (k_begin + i * TD_CHUNK));
-        const uint8_t* sk = td_smem + s * STAGE_BYTES;
-        const uint8_t* sv = sk + TD_CHUNK * D * 2;
-        uint4 kr[U], vr[U];
-        bool valid[U];
+        const int s = i % DM_STAGES;
+        mbar_wait(bar_full(s), (i / DM_STAGES) & 1);
+        const uint32_t sk = sbase + s * STAGE;
+        const uint32_t sv = sk + NB * DM_BOX;
+        const int nvalid = k_end - (k_begin + i * DM_CHUNK) - kb;  // keys of this warp's 16 that exist
+        if (nvalid > 0) {
+            // S = Q K^T over 16 keys (two n-tiles of 8)
+            float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int key = warp * KEYS_PER_WARP + u * KPW + sub;
-            valid[u] = key < nk;
-            const int kk = valid[u] ? key : 0;
-            kr[u] = *reinterpret_cast<const uint4*>(sk + kk * D * 2 + part * 16);
-            vr[u] = *reinterpret_cast<const uint4*>(sv + kk * D * 2 + part * 16);
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const int r = kb + (lane & 7) + ((lane >> 4) << 3);
+                const int c = ((ks & 3) << 1) + ((lane >> 3) & 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(sk + (ks >> 2) * DM_BOX + r * 128 + ((c ^ (r & 7)) << 4), b0, b1, b2, b3);
+                mma_bf16(sacc[0], qa[ks][0], 0u, qa[ks][1], 0u, b0, b1);
+                mma_bf16(sacc[1], qa[ks][0], 0u, qa[ks][1], 0u, b2, b3);
+            }
+            // online softmax for row gid (elements 0,1 of each n-tile; 2,3 are the padded rows)
+            float x[4];
+            x[0] = sacc[0][0] * sc; x[1] = sacc[0][1] * sc; x[2] = sacc[1][0] * sc; x[3] = sacc[1][1] * sc;
+            if (nvalid < 16) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if ((e >> 1) * 8 + tq * 2 + (e & 1) >= nvalid) x[e] = -CUDART_INF_F;
+            }
+            float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const bool grow = m_run == -CUDART_INF_F || mx > m_run + DM_RESCALE;
+            if (__any_sync(0xffffffffu, grow)) {
+                const float m_new = grow ? mx : m_run;
+                const float alpha = (m_run == -CUDART_INF_F) ? 0.f : fast_exp2(m_run - m_new);
+                l_run *= alpha;
+#pragma unroll
+                for (int nt = 0; nt < D / 8; ++nt) { o[nt][0] *= alpha; o[nt][1] *= alpha; }
+                m_run = m_new;
+            }
+            float pr[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                pr[e] = fast_exp2(x[e] - m_run);
+                l_run += pr[e];
+            }
+            const uint32_t pa0 = pack_bf16(pr[0], pr[1]);  // row gid, keys tq*2..   (k 0-7)
+            const uint32_t pa2 = pack_bf16(pr[2], pr[3]);  // row gid, keys 8+tq*2.. (k 8-15)
+            // O += P V (V rows = keys: transposed ldmatrix gives the k-major B fragments)
+#pragma unroll
+            for (int dn = 0; dn < D / 16; ++dn) {
+                const int r = kb + (lane & 7) + (((lane >> 3) & 1) << 3);
+                const int c = dn * 2 + (lane >> 4);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(sv + (c >> 3) * DM_BOX + r * 128 + (((c & 7) ^ (r & 7)) << 4), b0, b1, b2, b3);
+                mma_bf16(o[2 * dn], pa0, 0u, pa2, 0u, b0, b1);
+                mma_bf16(o[2 * dn + 1], pa0, 0u, pa2, 0u, b2, b3);
+            }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_empty(s));  // this warp's reads of stage s are done
-        float x[U][G];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            float kf[8];
-            bf16x8_to_f32(kr[u], kf);
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-                float acc = 0.f;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc = fmaf(q[j][e], kf[e], acc);
-                x[u][j] = acc;
-            }
-        }
-#pragma unroll
-        for (int off = 1; off < LPK; off <<= 1)
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int j = 0; j < G; ++j) x[u][j] += __shfl_xor_sync(0xffffffffu, x[u][j], off);
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-            float mx = m[j];
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (valid[u]) mx = fmaxf(mx, x[u][j]);
-            const float alpha = (m[j] == -CUDART_INF_F) ? 0.f : fast_exp2(m[j] - mx);
-            m[j] = mx;
-            l[j] *= alpha;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[j][e] *= alpha;
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (!valid[u]) continue;
-                const float pw = fast_exp2(x[u][j] - mx);
-                l[j] += pw;
-                float vf[8];
-                bf16x8_to_f32(vr[u], vf);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) o[j][e] = fmaf(pw, vf[e], o[j][e]);
-            }
-        }
+        if (lane == 0) mbar_arrive(bar_empty(s));
     }
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
 
-    // merge the KPW key slots of the warp (lanes with equal `part`)
-#pragma unroll
-    for (int off = LPK; off < 32; off <<= 1) {
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-            const float m2 = __shfl_xor_sync(0xffffffffu, m[j], off);
-            const float l2 = __shfl_xor_sync(0xffffffffu, l[j], off);
-            const float mx = fmaxf(m[j], m2);
-            const float a1 = (m[j] == -CUDART_INF_F) ? 0.f : fast_exp2(m[j] - mx);
-            const float a2 = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - mx);
-            l[j] = l[j] * a1 + l2 * a2;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float o2 = __shfl_xor_sync(0xffffffffu, o[j][e], off);
-                o[j][e] = o[j][e] * a1 + o2 * a2;
-            }
-            m[j] = mx;
-        }
-    }
     // merge the consumer warps through shared memory (the ring is free: every chunk was consumed)
-    float* sm_m = reinterpret_cast<float*>(td_smem);          // [NW][G]
-    float* sm_l = sm_m + NW * G;                              // [NW][G]
-    float* sm_o = sm_l + NW * G;                              // [NW][G][D]
-    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // all consumers done with the ring
-    if (sub == 0) {
+    float* sm_m = reinterpret_cast<float*>(smem);            // [W][G]
+    float* sm_l = sm_m + DM_CONSUMERS * G;                   // [W][G]
+    float* sm_o = sm_l + DM_CONSUMERS * G;                   // [W][G][D]
+    asm volatile("bar.sync 1, %0;" ::"n"(DM_CONSUMERS * 32) : "memory");
+    if (row_live) {
+        if (tq == 0) { sm_m[warp * G + gid] = m_run; sm_l[warp * G + gid] = l_run; }
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-            if (part == 0) { sm_m[warp * G + j] = m[j]; sm_l[warp * G + j] = l[j]; }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) sm_o[(warp * G + j) * D + part * 8 + e] = o[j][e];
+        for (int nt = 0; nt < D / 8; ++nt) {
+            sm_o[(warp * G + gid) * D + nt * 8 + tq * 2] = o[nt][0];
+            sm_o[(warp * G + gid) * D + nt * 8 + tq * 2 + 1] = o[nt][1];
         }
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(DM_CONSUMERS * 32) : "memory");
     float* rec = p.parts + static_cast<int64_t>(blockIdx.x) * G * (D + 4);
-    for (int idx = threadIdx.x; idx < G * D; idx += NW * 32) {
+    for (int idx = threadIdx.x; idx < G * D; idx += DM_CONSUMERS * 32) {
         const int j = idx / D, c = idx % D;
         float mx = -CUDART_INF_F;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) mx = fmaxf(mx, sm_m[w * G + j]);
+        for (int w = 0; w < DM_CONSUMERS; ++w) mx = fmaxf(mx, sm_m[w * G + j]);
         float lsum = 0.f, osum = 0.f;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
+        for (int w = 0; w < DM_CONSUMERS; ++w) {
             const float mw = sm_m[w * G + j];
             const float a = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - mx);
             lsum += a * sm_l[w * G + j];
@@ -328,16 +340,23 @@ __global__ void __launch_bounds__(CB_WARPS * 32) decode_combine_kernel(const Dec
 
 template <int D, int G>
 cudaError_t launch_partial_dg(const DecodePartialParams& p, int n_splits, cudaStream_t s) {
-    constexpr int smem = td_smem_bytes<D, G>();
+    constexpr int smem = dm_smem_bytes<D>();
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(decode_partial_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    decode_partial_kernel<D, G><<<n_splits, TD_THREADS, smem, s>>>(p);
+    CUtensorMap tk, tv;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(DM_CHUNK)};
+    if (!make_tmap_bf16(&tk, p.k, 2, dims, strides, box) || !make_tmap_bf16(&tv, p.v, 2, dims, strides, box))
+        return cudaErrorInvalidValue;
+    decode_partial_kernel<D, G><<<n_splits, DM_THREADS, smem, s>>>(tk, tv, p);
     return cudaGetLastError();
 }
+
 template <int D>
 cudaError_t launch_partial_d(const DecodePartialParams& p, int g, int n_splits, cudaStream_t s) {
     switch (g) {

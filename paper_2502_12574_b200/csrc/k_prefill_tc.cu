@@ -507,33 +507,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------- host side
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
-                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn get_encode() {
-    static EncodeFn fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* ptr = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeFn>(ptr);
-    });
-    return fn;
-}
-
-bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-            const cuuint32_t* box) {
-    EncodeFn fn = get_encode();
-    if (!fn) return false;
-    cuuint32_t es[3] = {1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides_bytes, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int D>
 cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
     const int n_rows = p.n_q * p.g;
@@ -550,14 +523,14 @@ cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
         const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.g), static_cast<cuuint64_t>(p.n_q)};
         const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(p.q_tok_stride) * 2};
         const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(p.g), static_cast<cuuint32_t>(BM / p.g)};
-        if (!encode(&tq, p.q, 3, dims, strides, box)) return cudaErrorInvalidValue;
+        if (!make_tmap_bf16(&tq, p.q, 3, dims, strides, box)) return cudaErrorInvalidValue;
     }
     {
         const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k)};
         const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.kv_row_stride) * 2};
         const cuuint32_t box[2] = {64, BN};
-        if (!encode(&tk, p.k, 2, dims, strides, box)) return cudaErrorInvalidValue;
-        if (!encode(&tv, p.v, 2, dims, strides, box)) return cudaErrorInvalidValue;
+        if (!make_tmap_bf16(&tk, p.k, 2, dims, strides, box)) return cudaErrorInvalidValue;
+        if (!make_tmap_bf16(&tv, p.v, 2, dims, strides, box)) return cudaErrorInvalidValue;
     }
     prefill_tc_kernel<D><<<grid, NUM_THREADS, Smem<D>::ALLOC, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();
