@@ -9,6 +9,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libheadinfer.so")
+# experiments only (tools/ab_prefill.sh): load a variant build of the same sources instead
+if os.environ.get("HI_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_HERE, "build", "variants", f"libheadinfer_{os.environ['HI_LIB_VARIANT']}.so")
 
 HI_OK, HI_EINVAL, HI_ESHAPE, HI_ECAPACITY, HI_ENOMEM_HOST, HI_ENOMEM_DEV, HI_ECUDA, HI_ESTATE = range(8)
 STATUS_NAMES = ["HI_OK", "HI_EINVAL", "HI_ESHAPE", "HI_ECAPACITY", "HI_ENOMEM_HOST", "HI_ENOMEM_DEV",

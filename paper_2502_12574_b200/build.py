@@ -60,6 +60,15 @@ def _nvcc_shared(out: str, srcs, extra=(), force=False, verbose=False):
     return out
 
 
+def build_variant(name: str, defines) -> str:
+    """Experiments: the same sources with extra -D flags -> build/variants/libheadinfer_<name>.so
+    (loaded when HI_LIB_VARIANT=<name>)."""
+    srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
+    out = os.path.join(PKG, "build", "variants", f"libheadinfer_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    return _nvcc_shared(out, srcs, extra=[f"-D{d}" for d in defines], force=True)
+
+
 def build(force: bool = False, verbose: bool = False) -> None:
     srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
     _nvcc_shared(os.path.join(PKG, "libheadinfer.so"), srcs, force=force, verbose=verbose)

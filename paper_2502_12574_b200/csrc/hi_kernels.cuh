@@ -55,8 +55,13 @@ struct DecodePartialParams {
     int split_len;            // keys per CTA
     float scale_log2;
     float* parts;             // records for this launch: parts + (blockIdx.x*g + j)*(d+4): {m, l, pad, pad, o[d]}
+    // several kv heads in one launch (blockIdx.y = head; HBM-resident heads, NEXT-1): per-head strides
+    int64_t kv_head_stride;   // elements between head h and h+1 in k and in v (0 when n_heads == 1)
+    int64_t q_head_stride;    // elements between the q groups of consecutive heads (g*d)
+    int64_t parts_head_stride;// floats between the record arrays of consecutive heads
 };
-cudaError_t launch_decode_partial(const DecodePartialParams& p, int d, int g, int n_splits, cudaStream_t stream);
+cudaError_t launch_decode_partial(const DecodePartialParams& p, int d, int g, int n_splits, int n_heads,
+                                  cudaStream_t stream);
 
 struct DecodeCombineParams {
     const __nv_bfloat16* q;      // [Hq_loc][d]

@@ -250,12 +250,14 @@ void destroy(hi_ctx* c) {
     delete c;
 }
 
-// Split length for the decode partial kernel (one 288-thread CTA per SM, TMA-fed ring): ~2 waves of
-// CTAs per history block, at least 64 keys (one ring stage) per CTA.
-int decode_split_len(int64_t nk) {
-    int64_t s = (nk + 2 * 148 - 1) / (2 * 148);
+// Split length for the decode partial kernel (one 160-thread CTA per SM, TMA-fed 6-stage ring): about
+// two waves of CTAs in total over the launch's `heads` kv heads, each CTA streaming one long contiguous
+// key range (a deep ring pays off only over many stages); at least 64 keys (one stage) per CTA.
+int decode_split_len(int64_t nk, int heads = 1) {
+    const int64_t target = std::max<int64_t>(1, (2 * 148 + heads - 1) / heads);
+    int64_t s = (nk + target - 1) / target;
     s = (s + 63) / 64 * 64;
-    return static_cast<int>(std::max<int64_t>(64, std::min<int64_t>(s, 1 << 20)));
+    return static_cast<int>(std::max<int64_t>(64, std::min<int64_t>(s, 1 << 30)));
 }
 int64_t decode_parts_for_block(int64_t nk) {
     const int sl = decode_split_len(nk);
@@ -653,27 +655,27 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     // history: per kv head, blocks through the slots -> split-K partial records
     const int64_t nb = (s + c->slot_tokens - 1) / c->slot_tokens;
     int n_parts_off = 0, n_parts_res = 0;
-    for (int h = 0; h < Hkv; ++h) {
+    const int r_l = c->resident_heads_of_layer(layer);
+    if (r_l > 0 && s > 0) {  // H_on heads of this layer: ONE split-K launch over [0, s) of all of them, in HBM
+        hi::DecodePartialParams p{};
+        p.q = static_cast<const __nv_bfloat16*>(q);
+        p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, 0, 0));
+        p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, 0, 0));
+        p.n_k = static_cast<int>(s);
+        p.split_len = decode_split_len(s, r_l);
+        p.scale_log2 = c->scale_log2;
+        p.parts = c->d_parts;
+        p.kv_head_stride = 2 * c->max_ctx * d;              // pairs are [K | V] blocks of max_ctx rows
+        p.q_head_stride = static_cast<int64_t>(g) * d;
+        p.parts_head_stride = static_cast<int64_t>(c->max_parts) * g * (d + 4);
+        n_parts_res = static_cast<int>((s + p.split_len - 1) / p.split_len);
+        LaunchTimer tm(c);
+        HI_CK(c, hi::launch_decode_partial(p, d, g, n_parts_res, r_l, c->s_comp));
+        tm.done(4.0 * d * static_cast<double>(s) * r_l, false);
+        ++c->launches;
+    }
+    for (int h = r_l; h < Hkv; ++h) {
         int pofs = 0;
-        if (c->resident(layer, h)) {  // H_on: one split-K pass over [0, s) in HBM
-            if (s > 0) {
-                hi::DecodePartialParams p{};
-                p.q = static_cast<const __nv_bfloat16*>(q) + static_cast<size_t>(h) * g * d;
-                p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, h, 0));
-                p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, h, 0));
-                p.n_k = static_cast<int>(s);
-                p.split_len = decode_split_len(s);
-                p.scale_log2 = c->scale_log2;
-                p.parts = c->d_parts + static_cast<size_t>(h) * c->max_parts * g * (d + 4);
-                pofs = static_cast<int>((s + p.split_len - 1) / p.split_len);
-                LaunchTimer tm(c);
-                HI_CK(c, hi::launch_decode_partial(p, d, g, pofs, c->s_comp));
-                tm.done(4.0 * d * static_cast<double>(s), false);
-                ++c->launches;
-            }
-            n_parts_res = pofs;
-            continue;
-        }
         for (int64_t b = 0; b < nb; ++b) {
             const int64_t k0 = b * c->slot_tokens;
             const int64_t nk = std::min<int64_t>(c->slot_tokens, s - k0);
@@ -691,7 +693,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
             const int nsp = static_cast<int>((nk + p.split_len - 1) / p.split_len);
             {
                 LaunchTimer tm(c);
-                HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, c->s_comp));
+                HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, 1, c->s_comp));
                 tm.done(4.0 * d * static_cast<double>(nk), false);
             }
             ++c->launches;

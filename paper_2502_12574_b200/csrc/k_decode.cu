@@ -67,6 +67,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
@@ -143,8 +149,8 @@ __global__ void __launch_bounds__(DM_THREADS, 1)
                 mbar_expect_tx(bar_full(s), STAGE);  // OOB rows of the last chunk are zero-filled, still counted
 #pragma unroll
                 for (int c = 0; c < NB; ++c) {
-                    tma_load_2d(sbase + s * STAGE + c * DM_BOX, &tm_k, bar_full(s), c * 64, k0);
-                    tma_load_2d(sbase + s * STAGE + (NB + c) * DM_BOX, &tm_v, bar_full(s), c * 64, k0);
+                    tma_load_3d(sbase + s * STAGE + c * DM_BOX, &tm_k, bar_full(s), c * 64, k0, blockIdx.y);
+                    tma_load_3d(sbase + s * STAGE + (NB + c) * DM_BOX, &tm_v, bar_full(s), c * 64, k0, blockIdx.y);
                 }
             }
         }
@@ -154,12 +160,13 @@ __global__ void __launch_bounds__(DM_THREADS, 1)
     // ---------------- consumers ----------------
     const int gid = lane >> 2, tq = lane & 3;
     const bool row_live = gid < G;
+    const __nv_bfloat16* qg = p.q + blockIdx.y * p.q_head_stride;
     // Q fragments (A operand, rows = q heads of the group, zero-padded to 16), all of D
     uint32_t qa[D / 16][2];  // {a0a1 (row gid, k 0-7 of the step), a4a5 (row gid, k 8-15)}; rows gid+8 are 0
 #pragma unroll
     for (int ks = 0; ks < D / 16; ++ks) {
-        qa[ks][0] = row_live ? *reinterpret_cast<const uint32_t*>(p.q + gid * D + ks * 16 + tq * 2) : 0u;
-        qa[ks][1] = row_live ? *reinterpret_cast<const uint32_t*>(p.q + gid * D + ks * 16 + 8 + tq * 2) : 0u;
+        qa[ks][0] = row_live ? *reinterpret_cast<const uint32_t*>(qg + gid * D + ks * 16 + tq * 2) : 0u;
+        qa[ks][1] = row_live ? *reinterpret_cast<const uint32_t*>(qg + gid * D + ks * 16 + 8 + tq * 2) : 0u;
     }
     float o[D / 8][4];
 #pragma unroll
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(DM_THREADS, 1)
         }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(DM_CONSUMERS * 32) : "memory");
-    float* rec = p.parts + static_cast<int64_t>(blockIdx.x) * G * (D + 4);
+    float* rec = p.parts + blockIdx.y * p.parts_head_stride + static_cast<int64_t>(blockIdx.x) * G * (D + 4);
     for (int idx = threadIdx.x; idx < G * D; idx += DM_CONSUMERS * 32) {
         const int j = idx / D, c = idx % D;
         float mx = -CUDART_INF_F;
@@ -339,7 +346,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32) decode_combine_kernel(const Dec
 }
 
 template <int D, int G>
-cudaError_t launch_partial_dg(const DecodePartialParams& p, int n_splits, cudaStream_t s) {
+cudaError_t launch_partial_dg(const DecodePartialParams& p, int n_splits, int n_heads, cudaStream_t s) {
     constexpr int smem = dm_smem_bytes<D>();
     static bool configured = false;
     if (!configured) {
@@ -348,32 +355,34 @@ cudaError_t launch_partial_dg(const DecodePartialParams& p, int n_splits, cudaSt
         configured = true;
     }
     CUtensorMap tk, tv;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
-    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(DM_CHUNK)};
-    if (!make_tmap_bf16(&tk, p.k, 2, dims, strides, box) || !make_tmap_bf16(&tv, p.v, 2, dims, strides, box))
+    const int64_t hs = n_heads > 1 ? p.kv_head_stride : static_cast<int64_t>(p.n_k) * D;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k), static_cast<cuuint64_t>(n_heads)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(hs) * 2};
+    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(DM_CHUNK), 1};
+    if (!make_tmap_bf16(&tk, p.k, 3, dims, strides, box) || !make_tmap_bf16(&tv, p.v, 3, dims, strides, box))
         return cudaErrorInvalidValue;
-    decode_partial_kernel<D, G><<<n_splits, DM_THREADS, smem, s>>>(tk, tv, p);
+    decode_partial_kernel<D, G><<<dim3(n_splits, n_heads), DM_THREADS, smem, s>>>(tk, tv, p);
     return cudaGetLastError();
 }
 
 template <int D>
-cudaError_t launch_partial_d(const DecodePartialParams& p, int g, int n_splits, cudaStream_t s) {
+cudaError_t launch_partial_d(const DecodePartialParams& p, int g, int n_splits, int n_heads, cudaStream_t s) {
     switch (g) {
-        case 1: return launch_partial_dg<D, 1>(p, n_splits, s);
-        case 2: return launch_partial_dg<D, 2>(p, n_splits, s);
-        case 4: return launch_partial_dg<D, 4>(p, n_splits, s);
-        case 8: return launch_partial_dg<D, 8>(p, n_splits, s);
+        case 1: return launch_partial_dg<D, 1>(p, n_splits, n_heads, s);
+        case 2: return launch_partial_dg<D, 2>(p, n_splits, n_heads, s);
+        case 4: return launch_partial_dg<D, 4>(p, n_splits, n_heads, s);
+        case 8: return launch_partial_dg<D, 8>(p, n_splits, n_heads, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
 }  // namespace
 
-cudaError_t launch_decode_partial(const DecodePartialParams& p, int d, int g, int n_splits, cudaStream_t stream) {
-    if (n_splits <= 0) return cudaSuccess;
-    if (d == 64) return launch_partial_d<64>(p, g, n_splits, stream);
-    if (d == 128) return launch_partial_d<128>(p, g, n_splits, stream);
+cudaError_t launch_decode_partial(const DecodePartialParams& p, int d, int g, int n_splits, int n_heads,
+                                  cudaStream_t stream) {
+    if (n_splits <= 0 || n_heads <= 0) return cudaSuccess;
+    if (d == 64) return launch_partial_d<64>(p, g, n_splits, n_heads, stream);
+    if (d == 128) return launch_partial_d<128>(p, g, n_splits, n_heads, stream);
     return cudaErrorInvalidValue;
 }
 

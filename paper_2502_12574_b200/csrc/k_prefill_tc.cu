@@ -39,7 +39,10 @@ constexpr int BN = 128;            // keys per KV tile
 constexpr int NS = 2;              // K/V pipeline stages
 constexpr int NUM_THREADS = 384;   // 2 x 4 softmax warps (one Q tile each) + TMA warp + MMA warp + 2 spare
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
-constexpr int EX2_POLY_EVERY = 16;         // 2 of every 16 exponentials on the FMA pipe (see ex2_poly)
+#ifndef HI_EX2_POLY_EVERY
+#define HI_EX2_POLY_EVERY 16
+#endif
+constexpr int EX2_POLY_EVERY = HI_EX2_POLY_EVERY;  // 2 of every 16 exponentials on the FMA pipe (see ex2_poly)
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -296,25 +299,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
             const int nk_t[2] = {n_kt0, n_kt1};
             mbar_wait(bar_q, 0);
+            // descriptors precomputed once; a K-step / stage offset is added to the 14-bit start-address
+            // field (shared-memory addresses < 256 KiB, so the field never carries)
+            const uint64_t dq0 = sdesc(sbase + L::Q_OFF, 16, 1024);
+            const uint64_t dk0 = sdesc(sbase + L::K_OFF, 16, 1024);
+            const uint64_t dv0 = sdesc(sbase + L::V_OFF, L::BOX, 1024);
             auto issue_s = [&](int tt, int i) {  // S_tt(i) = Q_tt K(i)^T
                 const int s = i % NS;
+                const uint64_t a0 = dq0 + ((tt * (D / 64) * L::BOX) >> 4);
+                const uint64_t b0 = dk0 + ((s * (D / 64) * L::BOX) >> 4);
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
-                    const uint32_t off = (ks >> 2) * L::BOX + (ks & 3) * 32;
-                    const uint64_t a = sdesc(sbase + L::Q_OFF + tt * (D / 64) * L::BOX + off, 16, 1024);
-                    const uint64_t b = sdesc(sbase + L::K_OFF + s * (D / 64) * L::BOX + off, 16, 1024);
-                    umma_bf16(tmem + tt * 256, a, b, ID_S, ks > 0);
+                    const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
+                    umma_bf16(tmem + tt * 256, a0 + off, b0 + off, ID_S, ks > 0);
                 }
                 umma_commit(bar_s(tt));
             };
             auto issue_pv = [&](int tt, int j) {  // O_tt += P_tt(j) V(j), P from TMEM
                 const int s = j % NS;
+                const uint64_t b0 = dv0 + ((s * (D / 64) * L::BOX) >> 4);
 #pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk) {
-                    const uint64_t b = sdesc(sbase + L::V_OFF + s * (D / 64) * L::BOX + kk * 16 * 128, L::BOX, 1024);
-                    umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, b, ID_O,
+                for (int kk = 0; kk < BN / 16; ++kk)
+                    umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                  (j > 0 || kk > 0 || !first) ? 1u : 0u);
-                }
                 if (j + 1 == nk_t[tt]) umma_commit(bar_o(tt));  // O final: the epilogue's only wait
             };
             mbar_wait(bar_k(0), 0);
