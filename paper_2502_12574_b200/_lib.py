@@ -81,6 +81,9 @@ def load() -> ctypes.CDLL:
     lib.hi_status_str.restype = ctypes.c_char_p
     lib.hi_last_error.argtypes = [P]
     lib.hi_last_error.restype = ctypes.c_char_p
+    if hasattr(lib, "hi_debug_prefill_trace"):  # HI_TRACE variant builds only
+        lib.hi_debug_prefill_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+        lib.hi_debug_prefill_trace.restype = ctypes.c_int
     for name in ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",
                  "hi_write_host_kv", "hi_set_seq_len", "hi_get_stats", "hi_synchronize"]:
         getattr(lib, name).restype = I

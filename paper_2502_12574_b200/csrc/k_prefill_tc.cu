@@ -39,6 +39,15 @@ constexpr int BN = 128;            // keys per KV tile
 constexpr int NS = 2;              // K/V pipeline stages
 constexpr int NUM_THREADS = 384;   // 2 x 4 softmax warps (one Q tile each) + TMA warp + MMA warp + 2 spare
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+
+// Optional timeline trace (variant builds with -DHI_TRACE): clock64() at pipeline events of CTA 0,
+// read back with hi_debug_prefill_trace(); off in the product build.
+#ifdef HI_TRACE
+__device__ unsigned long long g_hi_trace[16][512];
+#define HI_TR(ev, j) do { if (blockIdx.x == 0 && (threadIdx.x & 127) == 0 && (j) < 512) g_hi_trace[ev][j] = clock64(); } while (0)
+#else
+#define HI_TR(ev, j) do { } while (0)
+#endif
 #ifndef HI_EX2_POLY_EVERY
 #define HI_EX2_POLY_EVERY 16
 #endif
@@ -334,6 +343,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int tt = 0; tt < n_tiles; ++tt) {
                     if (j >= nk_t[tt]) continue;
                     mbar_wait(bar_p(tt), j & 1);
+                    HI_TR(12 + 2 * tt, j);
                     if (!waited_v) { mbar_wait(bar_v(s), (j / NS) & 1); waited_v = true; }
                     tc_fence_after();
                     issue_pv(tt, j);
@@ -341,6 +351,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (!waited_k) { mbar_wait(bar_k((j + 1) % NS), ((j + 1) / NS) & 1); waited_k = true; }
                         tc_fence_after();
                         issue_s(tt, j + 1);
+                        HI_TR(12 + 2 * tt + 1, j);
                     }
                 }
                 umma_commit(bar_e(s));  // K(j), V(j) consumed by every tile
@@ -350,7 +361,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ====================== softmax / correction / epilogue: warps 0-3 tile 0, 4-7 tile 1 ======================
         setmaxnreg_inc_208();
         const int tt = warp >> 2;
-        const int wq = warp & 3;                  // TMEM lane quarter
+        const int wq = warp & 3;
+        const int ttr = tt * 5;  // trace slot base (HI_TRACE builds)
+        (void)ttr;                  // TMEM lane quarter
         const int r = wq * 32 + lane;             // row within the tile == TMEM lane
         const int rg = row0 + tt * BM + r;        // packed row index t*g + j
         const bool row_valid = rg < n_rows;
@@ -385,12 +398,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             for (int j = 0; j < nkt; ++j) {
                 mbar_wait(bar_s(tt), j & 1);   // also implies PV(j-1) of this tile is complete (in-order MMAs)
+                HI_TR(10 + tt, j);
                 tc_fence_after();
                 uint32_t x[BN];
 #pragma unroll
                 for (int cb = 0; cb < BN / 32; ++cb)
                     tmem_ld32(t_s + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[cb * 32]));
                 tmem_wait_ld();
+                HI_TR(ttr + 0, j);
                 // row max of the raw scores (scale > 0 commutes with max); masking where needed
                 const int key0 = j * BN;
                 const bool need_mask = (key0 + BN > p.n_k) || (causal && p.k_pos0 + key0 + BN - 1 > p.q_pos0 + t_lo);
@@ -411,6 +426,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int c = 0; c < 8; ++c) mk[c] = fmaxf(mk[c], __uint_as_float(x[i + c]));
                 float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])), fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
                 const float mxs = mx * sc;  // log2-domain tile max
+                HI_TR(ttr + 1, j);
                 // lazy rescale: move the reference max only when it grows by > 2^8
                 float m_ref = m_run, alpha = 1.f;
                 const bool grow = (mx != -CUDART_INF_F) && (m_run == -CUDART_INF_F || mxs > m_run + RESCALE_THRESHOLD);
@@ -432,6 +448,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     x[i / 2] = pack_bf16(p0, p1);
                 }
                 const float lsum0 = (ls[0] + ls[1]), lsum1 = (ls[2] + ls[3]);
+                HI_TR(ttr + 2, j);
                 // P -> TMEM (overwrites the consumed S columns of this row)
                 tmem_st32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
                 tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));
@@ -448,10 +465,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
                 tmem_wait_st();
+                HI_TR(ttr + 3, j);
                 l_run = l_run * alpha + (lsum0 + lsum1);
                 m_run = m_ref;
                 tc_fence_before();
                 mbar_arrive(bar_p(tt));
+                HI_TR(ttr + 4, j);
             }
             // ---- epilogue ----
             if (nkt > 0) {
@@ -544,6 +563,12 @@ cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
 }
 
 }  // namespace
+
+#ifdef HI_TRACE
+extern "C" int hi_debug_prefill_trace(void* dst, size_t bytes) {
+    return static_cast<int>(cudaMemcpyFromSymbol(dst, g_hi_trace, bytes));
+}
+#endif
 
 cudaError_t launch_prefill_tc(const PrefillParams& p, int d, cudaStream_t stream) {
     if (d == 64) return launch_tc<64>(p, stream);
