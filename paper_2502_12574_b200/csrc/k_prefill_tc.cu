@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <cstdio>
 #include <mutex>
 
 namespace hi {
@@ -37,7 +38,35 @@ namespace {
 constexpr int BM = 128;            // query rows per CTA (TMEM lanes)
 constexpr int BN = 128;            // keys per KV tile
 constexpr int NS = 2;              // K/V pipeline stages
-constexpr int NUM_THREADS = 384;   // 2 x 4 softmax warps (one Q tile each) + TMA warp + MMA warp + 2 spare
+#ifndef HI_SOFTMAX_SPLIT
+#define HI_SOFTMAX_SPLIT 1
+#endif
+#ifndef HI_SPEC_EXP
+#define HI_SPEC_EXP 0  // measured: no gain (profiles/ab_prefill_r01.txt)
+#endif
+constexpr bool SPEC_EXP = HI_SPEC_EXP != 0;
+// SPLIT softmax warps per TMEM lane quarter and tile, each owning BN/SPLIT S columns of its rows
+// (and D/SPLIT O columns).  MUFU ex2 issues at 4 lanes/clk/SMSP (profiles/ubench_xu_rate_r01.txt), so
+// with one softmax warp per SMSP and tile the exponentials of a 128 x 128 tile alone take 1024 cycles
+// = the tensor time of PV + the next QK^T; a second warp per SMSP lets the FMA-pipe polynomial of one
+// warp issue while the other waits on MUFU, and halves each warp's serial chain.
+constexpr int SPLIT = HI_SOFTMAX_SPLIT;
+constexpr int SOFTMAX_WARPS = 8 * SPLIT;
+constexpr int WARP_TMA = SOFTMAX_WARPS, WARP_MMA = SOFTMAX_WARPS + 1;
+constexpr int NUM_THREADS = 32 * (SOFTMAX_WARPS + 4);  // + one warpgroup: TMA warp, MMA warp, 2 idle
+// Register budget (setmaxnreg).  setmaxnreg.inc only draws on registers that setmaxnreg.dec released
+// in the same CTA (it blocks forever otherwise), so  softmax threads x (inc - launch)  must equal at
+// most  producer threads x (launch - dec):
+//   SPLIT=1: launch 168 x 384; softmax 208 (+40 x 256), producer 88 (-80 x 128)
+//   SPLIT=2: launch  96 x 640; softmax 104 (+8 x 512), producer 64 (-32 x 128)
+#ifndef HI_REG_SOFTMAX
+#define HI_REG_SOFTMAX (SPLIT == 1 ? 208 : 104)
+#endif
+#ifndef HI_REG_PRODUCER
+#define HI_REG_PRODUCER (SPLIT == 1 ? 88 : 64)
+#endif
+constexpr int REG_SOFTMAX = HI_REG_SOFTMAX;
+constexpr int REG_PRODUCER = HI_REG_PRODUCER;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 // Optional timeline trace (variant builds with -DHI_TRACE): clock64() at pipeline events of CTA 0,
@@ -45,11 +74,13 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #ifdef HI_TRACE
 __device__ unsigned long long g_hi_trace[16][512];
 #define HI_TR(ev, j) do { if (blockIdx.x == 0 && (threadIdx.x & 127) == 0 && (j) < 512) g_hi_trace[ev][j] = clock64(); } while (0)
+#define HI_TR_MMA(ev, j) do { if (blockIdx.x == 0 && (j) < 512) g_hi_trace[ev][j] = clock64(); } while (0)
 #else
 #define HI_TR(ev, j) do { } while (0)
+#define HI_TR_MMA(ev, j) do { } while (0)
 #endif
 #ifndef HI_EX2_POLY_EVERY
-#define HI_EX2_POLY_EVERY 16
+#define HI_EX2_POLY_EVERY 1000000  // off: MUFU + polynomial measured slower (profiles/ab_prefill_r01.txt)
 #endif
 constexpr int EX2_POLY_EVERY = HI_EX2_POLY_EVERY;  // 2 of every 16 exponentials on the FMA pipe (see ex2_poly)
 
@@ -82,7 +113,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "r"(bar), "r"(parity)
             : "memory");
         if (done) return;
+#ifdef HI_DEBUG_WAIT
+        if (it > (1u << 22)) {
+            printf("mbar_wait timeout: cta %d warp %d lane %d bar_off 0x%x parity %u\n", blockIdx.x, threadIdx.x / 32,
+                   threadIdx.x % 32, bar & 0xfff, parity);
+            __trap();
+        }
+#else
         if (it > (1u << 31)) __trap();
+#endif
     }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
@@ -198,6 +237,9 @@ struct __align__(8) Barriers {
     uint64_t k_full[NS], v_full[NS], kv_empty[NS];
     uint64_t s_full[2], p_full[2], o_done[2];
     uint32_t tmem_base;
+    uint32_t pad;
+    float xchg[2][2][BM];   // [tile][half][row]: partial row max, SPLIT=2
+    float xchg_l[2][2][BM]; // [tile][half][row]: partial row sum (epilogue), SPLIT=2
 };
 
 template <int D>
@@ -207,14 +249,19 @@ struct Smem {
     static constexpr int K_OFF = Q_OFF + 2 * (D / 64) * BOX;
     static constexpr int V_OFF = K_OFF + NS * (D / 64) * BOX;
     static constexpr int BAR_OFF = V_OFF + NS * (D / 64) * BOX;
-    static constexpr int BYTES = BAR_OFF + 256;
+    static constexpr int BYTES = BAR_OFF + static_cast<int>(sizeof(Barriers));
     static constexpr int ALLOC = BYTES + 1024;      // slack for 1 KiB alignment
 };
 
-// Register budget: the launch grants 168 regs x 384 threads; setmaxnreg.inc blocks until the pool
-// can satisfy it, so 2 x 128 x 208 (softmax) + 128 x 88 (TMA/MMA group) must be <= 168 x 384.
-__device__ __forceinline__ void setmaxnreg_inc_208() { asm volatile("setmaxnreg.inc.sync.aligned.u32 208;"); }
-__device__ __forceinline__ void setmaxnreg_dec_88() { asm volatile("setmaxnreg.dec.sync.aligned.u32 88;"); }
+__device__ __forceinline__ void setmaxnreg_softmax() {
+    if constexpr (REG_SOFTMAX > (SPLIT == 1 ? 168 : 96)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_SOFTMAX));
+}
+__device__ __forceinline__ void setmaxnreg_producer() {
+    if constexpr (REG_PRODUCER < (SPLIT == 1 ? 168 : 96)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_PRODUCER));
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 // TMEM column map (512 allocated): tile tt in {0,1}: S/P at [256*tt, 256*tt+128), O at [256*tt+128, +D).
 // P (bf16, packed in pairs) overwrites the first 64 columns of S after the row has been read.
@@ -268,12 +315,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(bar_s(t), 1);
-            mbar_init(bar_p(t), 128);
+            mbar_init(bar_p(t), 128 * SPLIT);
             mbar_init(bar_o(t), 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 9) {
+    if (warp == WARP_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&bars->tmem_base))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -283,9 +330,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
 
-    if (warp >= 8) {
-        setmaxnreg_dec_88();
-        if (warp == 8 && lane == 0 && n_kt > 0) {
+    if (warp >= SOFTMAX_WARPS) {
+        setmaxnreg_producer();
+        if (warp == WARP_TMA && lane == 0 && n_kt > 0) {
             // ============================ TMA producer ============================
             mbar_expect_tx(bar_q, n_tiles * (D / 64) * L::BOX);
             for (int tt = 0; tt < n_tiles; ++tt)
@@ -302,7 +349,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int c = 0; c < D / 64; ++c)
                     tma_load_2d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, i * BN);
             }
-        } else if (warp == 9 && lane == 0 && n_kt > 0) {
+        } else if (warp == WARP_MMA && lane == 0 && n_kt > 0) {
             // ============================ MMA issuer ==============================
             constexpr uint32_t ID_S = idesc_bf16(BM, BN, false);
             constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
@@ -317,20 +364,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const int s = i % NS;
                 const uint64_t a0 = dq0 + ((tt * (D / 64) * L::BOX) >> 4);
                 const uint64_t b0 = dk0 + ((s * (D / 64) * L::BOX) >> 4);
+#ifndef HI_SKIP_S  // timing experiment switch
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
                     umma_bf16(tmem + tt * 256, a0 + off, b0 + off, ID_S, ks > 0);
                 }
+#endif
                 umma_commit(bar_s(tt));
             };
             auto issue_pv = [&](int tt, int j) {  // O_tt += P_tt(j) V(j), P from TMEM
                 const int s = j % NS;
                 const uint64_t b0 = dv0 + ((s * (D / 64) * L::BOX) >> 4);
+#ifndef HI_SKIP_PV  // timing experiment switch
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk)
                     umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                  (j > 0 || kk > 0 || !first) ? 1u : 0u);
+#endif
                 if (j + 1 == nk_t[tt]) umma_commit(bar_o(tt));  // O final: the epilogue's only wait
             };
             mbar_wait(bar_k(0), 0);
@@ -343,7 +394,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int tt = 0; tt < n_tiles; ++tt) {
                     if (j >= nk_t[tt]) continue;
                     mbar_wait(bar_p(tt), j & 1);
-                    HI_TR(12 + 2 * tt, j);
+                    HI_TR_MMA(12 + 2 * tt, j);
                     if (!waited_v) { mbar_wait(bar_v(s), (j / NS) & 1); waited_v = true; }
                     tc_fence_after();
                     issue_pv(tt, j);
@@ -351,7 +402,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (!waited_k) { mbar_wait(bar_k((j + 1) % NS), ((j + 1) / NS) & 1); waited_k = true; }
                         tc_fence_after();
                         issue_s(tt, j + 1);
-                        HI_TR(12 + 2 * tt + 1, j);
+                        HI_TR_MMA(12 + 2 * tt + 1, j);
                     }
                 }
                 umma_commit(bar_e(s));  // K(j), V(j) consumed by every tile
@@ -359,13 +410,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else {
         // ====================== softmax / correction / epilogue: warps 0-3 tile 0, 4-7 tile 1 ======================
-        setmaxnreg_inc_208();
-        const int tt = warp >> 2;
-        const int wq = warp & 3;
+        setmaxnreg_softmax();
+        const int tt = warp / (4 * SPLIT);
+        const int hf = (warp / 4) % SPLIT;          // which BN/SPLIT S columns (and D/SPLIT O columns)
+        const int wq = warp & 3;                    // TMEM lane quarter
         const int ttr = tt * 5;  // trace slot base (HI_TRACE builds)
-        (void)ttr;                  // TMEM lane quarter
-        const int r = wq * 32 + lane;             // row within the tile == TMEM lane
-        const int rg = row0 + tt * BM + r;        // packed row index t*g + j
+        (void)ttr;
+        constexpr int HN = BN / SPLIT;              // S columns per thread
+        constexpr int HD = D / SPLIT;               // O columns per thread
+        const int r = wq * 32 + lane;               // row within the tile == TMEM lane
+        const int rg = row0 + tt * BM + r;          // packed row index t*g + j
         const bool row_valid = rg < n_rows;
         const int t = row_valid ? rg / g : 0;
         const int64_t qpos = p.q_pos0 + t;
@@ -373,18 +427,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int t_lo = (row0 + tt * BM) / g;
         const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
         const uint32_t t_s = tmem + tt * 256 + lane_addr;        // S / P columns of this row
-        const uint32_t t_o = t_s + 128;                          // O columns of this row
+        const uint32_t t_o = t_s + 128 + hf * HD;                // this thread's O columns
+        float* x_mine = &bars->xchg[tt][hf][r];
+        const float* x_other = &bars->xchg[tt][hf ^ 1][r];
         const float sc = p.scale_log2;
-        float m_run = -CUDART_INF_F, l_run = 0.f;
+        float m_run = -CUDART_INF_F, l_run = 0.f;  // l_run: this thread's partial row sum
         if (tt < n_tiles) {
             if (!first) {
                 m_run = row_valid ? p.m_acc[rg] : -CUDART_INF_F;
-                l_run = row_valid ? p.l_acc[rg] : 0.f;
+                l_run = (row_valid && hf == 0) ? p.l_acc[rg] : 0.f;
                 if (nkt > 0) {  // running O -> TMEM before the first PV accumulates onto it
 #pragma unroll
-                    for (int cb = 0; cb < D / 32; ++cb) {
+                    for (int cb = 0; cb < HD / 32; ++cb) {
                         uint32_t v[32];
-                        const float4* src = reinterpret_cast<const float4*>(p.o_acc + static_cast<int64_t>(row_valid ? rg : 0) * D + cb * 32);
+                        const float4* src = reinterpret_cast<const float4*>(
+                            p.o_acc + static_cast<int64_t>(row_valid ? rg : 0) * D + hf * HD + cb * 32);
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
                             float4 f = row_valid ? src[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -400,46 +457,100 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 mbar_wait(bar_s(tt), j & 1);   // also implies PV(j-1) of this tile is complete (in-order MMAs)
                 HI_TR(10 + tt, j);
                 tc_fence_after();
-                uint32_t x[BN];
+                uint32_t x[HN];
 #pragma unroll
-                for (int cb = 0; cb < BN / 32; ++cb)
-                    tmem_ld32(t_s + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[cb * 32]));
+                for (int cb = 0; cb < HN / 32; ++cb)
+                    tmem_ld32(t_s + hf * HN + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[cb * 32]));
                 tmem_wait_ld();
                 HI_TR(ttr + 0, j);
                 // row max of the raw scores (scale > 0 commutes with max); masking where needed
-                const int key0 = j * BN;
-                const bool need_mask = (key0 + BN > p.n_k) || (causal && p.k_pos0 + key0 + BN - 1 > p.q_pos0 + t_lo);
+                const int key0 = j * BN + hf * HN;
+                const bool need_mask = (j * BN + BN > p.n_k) || (causal && p.k_pos0 + j * BN + BN - 1 > p.q_pos0 + t_lo);
                 if (need_mask) {
                     const int64_t lim = causal ? qpos - p.k_pos0 : static_cast<int64_t>(p.n_k) - 1;
                     const int64_t lim2 = lim < p.n_k - 1 ? lim : static_cast<int64_t>(p.n_k) - 1;
 #pragma unroll
-                    for (int i = 0; i < BN; ++i)
+                    for (int i = 0; i < HN; ++i)
                         if (key0 + i > lim2) x[i] = __float_as_uint(-CUDART_INF_F);
                 }
+                float m_ref = m_run, alpha = 1.f;
+                bool grow = false;
+                float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#ifdef HI_FAKE_SOFTMAX  // timing experiment only: tensor-core / pipeline bound without the softmax math
+                tc_fence_before();
+                mbar_arrive(bar_p(tt));
+                continue;
+#endif
+                // Speculative pass (SPLIT == 1): exponentiate against the CURRENT reference max while the
+                // tile max is reduced alongside, so the max is off the critical path.  With lazy rescaling the
+                // reference moves only when a row max grows by > 2^8; then (rarely) the warp re-reads S from
+                // TMEM (still intact: P is not stored yet) and redoes the pass with the new reference.
+                bool done = false;
+                if constexpr (SPLIT == 1 && SPEC_EXP) {
+                    if (__all_sync(0xffffffffu, m_run != -CUDART_INF_F)) {
+                        const float neg_m = -m_run;
+                        float mk[8];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) mk[c] = -CUDART_INF_F;
+#pragma unroll
+                        for (int i = 0; i < HN; i += 2) {
+                            const float r0 = __uint_as_float(x[i]), r1 = __uint_as_float(x[i + 1]);
+                            mk[(i >> 1) & 7] = fmaxf(mk[(i >> 1) & 7], fmaxf(r0, r1));
+                            const float p0 = ex2(fmaf(r0, sc, neg_m));
+                            const float p1 = ex2(fmaf(r1, sc, neg_m));
+                            ls[(i >> 1) & 3] += p0 + p1;
+                            x[i / 2] = pack_bf16(p0, p1);
+                        }
+                        const float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
+                                               fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
+                        grow = (mx != -CUDART_INF_F) && (mx * sc > m_run + RESCALE_THRESHOLD);
+                        done = !__any_sync(0xffffffffu, grow);
+                        if (!done) {  // re-read S (TMEM untouched) for the slow path
+                            ls[0] = ls[1] = ls[2] = ls[3] = 0.f;
+#pragma unroll
+                            for (int cb = 0; cb < HN / 32; ++cb)
+                                tmem_ld32(t_s + hf * HN + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[cb * 32]));
+                            tmem_wait_ld();
+                            if (need_mask) {
+                                const int64_t lim = causal ? qpos - p.k_pos0 : static_cast<int64_t>(p.n_k) - 1;
+                                const int64_t lim2 = lim < p.n_k - 1 ? lim : static_cast<int64_t>(p.n_k) - 1;
+#pragma unroll
+                                for (int i = 0; i < HN; ++i)
+                                    if (key0 + i > lim2) x[i] = __float_as_uint(-CUDART_INF_F);
+                            }
+                        }
+                    }
+                }
+                if (!done) {
                 // 8 independent max chains (short dependency chain), then combine
                 float mk[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) mk[c] = __uint_as_float(x[c]);
 #pragma unroll
-                for (int i = 8; i < BN; i += 8)
+                for (int i = 8; i < HN; i += 8)
 #pragma unroll
                     for (int c = 0; c < 8; ++c) mk[c] = fmaxf(mk[c], __uint_as_float(x[i + c]));
                 float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])), fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
-                const float mxs = mx * sc;  // log2-domain tile max
+                if constexpr (SPLIT == 2) {
+                    // combine the two halves' maxima; after this barrier both halves have finished reading
+                    // S, so P may overwrite any S column of the row
+                    *x_mine = mx;
+                    named_bar_sync(1 + tt, 256);
+                    mx = fmaxf(mx, *x_other);
+                }
                 HI_TR(ttr + 1, j);
+                const float mxs = mx * sc;  // log2-domain tile max
                 // lazy rescale: move the reference max only when it grows by > 2^8
-                float m_ref = m_run, alpha = 1.f;
-                const bool grow = (mx != -CUDART_INF_F) && (m_run == -CUDART_INF_F || mxs > m_run + RESCALE_THRESHOLD);
+                grow = (mx != -CUDART_INF_F) && (m_run == -CUDART_INF_F || mxs > m_run + RESCALE_THRESHOLD);
                 if (grow) {
                     m_ref = mxs;
                     alpha = (m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mxs);
                 }
                 const float neg_m = (m_ref == -CUDART_INF_F) ? 0.f : -m_ref;
-                float ls[4] = {0.f, 0.f, 0.f, 0.f};
-                // p = 2^(x*scale - m): packed to bf16 pairs in place (x[i/2] is dead once read).  One
-                // element in EX2_POLY_EVERY goes through the FMA-pipe polynomial, the rest through MUFU.
+                // p = 2^(x*scale - m): packed to bf16 pairs in place (x[i/2] is dead once read).  Two
+                // elements in EX2_POLY_EVERY go through the FMA-pipe polynomial, the rest through MUFU.
 #pragma unroll
-                for (int i = 0; i < BN; i += 2) {
+                for (int i = 0; i < HN; i += 2) {
                     const float a0 = fmaf(__uint_as_float(x[i]), sc, neg_m);
                     const float a1 = fmaf(__uint_as_float(x[i + 1]), sc, neg_m);
                     const float p0 = ((i % EX2_POLY_EVERY) == EX2_POLY_EVERY - 2) ? ex2_poly(a0) : ex2(a0);
@@ -447,15 +558,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ls[(i >> 1) & 3] += p0 + p1;
                     x[i / 2] = pack_bf16(p0, p1);
                 }
-                const float lsum0 = (ls[0] + ls[1]), lsum1 = (ls[2] + ls[3]);
+                }
                 HI_TR(ttr + 2, j);
-                // P -> TMEM (overwrites the consumed S columns of this row)
-                tmem_st32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
-                tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));
+                // P -> TMEM: this thread's keys are packed columns [hf*HN/2, (hf+1)*HN/2)
+#pragma unroll
+                for (int cb = 0; cb < HN / 64; ++cb)
+                    tmem_st32(t_s + hf * (HN / 2) + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[cb * 32]));
                 const bool o_live = !first || j > 0;
                 if (o_live && __any_sync(0xffffffffu, grow)) {
 #pragma unroll
-                    for (int cb = 0; cb < D / 32; ++cb) {
+                    for (int cb = 0; cb < HD / 32; ++cb) {
                         uint32_t v[32];
                         tmem_ld32(t_o + cb * 32, v);
                         tmem_wait_ld();
@@ -466,22 +578,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 tmem_wait_st();
                 HI_TR(ttr + 3, j);
-                l_run = l_run * alpha + (lsum0 + lsum1);
+                l_run = l_run * alpha + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
                 m_run = m_ref;
                 tc_fence_before();
                 mbar_arrive(bar_p(tt));
                 HI_TR(ttr + 4, j);
             }
             // ---- epilogue ----
+            float l_tot = l_run;
+            if constexpr (SPLIT == 2) {
+                bars->xchg_l[tt][hf][r] = l_run;
+                named_bar_sync(1 + tt, 256);
+                l_tot += bars->xchg_l[tt][hf ^ 1][r];
+            }
             if (nkt > 0) {
                 mbar_wait(bar_o(tt), 0);
                 tc_fence_after();
             }
             if (last) {
-                const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (rg % g) * D;
+                const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (rg % g) * D + hf * HD;
 #pragma unroll
-                for (int cb = 0; cb < D / 32; ++cb) {
+                for (int cb = 0; cb < HD / 32; ++cb) {
                     uint32_t v[32];
                     if (nkt > 0) {
                         tmem_ld32(t_o + cb * 32, v);
@@ -489,7 +607,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     } else {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
-                            v[i] = (row_valid && !first) ? __float_as_uint(p.o_acc[static_cast<int64_t>(rg) * D + cb * 32 + i]) : 0u;
+                            v[i] = (row_valid && !first)
+                                       ? __float_as_uint(p.o_acc[static_cast<int64_t>(rg) * D + hf * HD + cb * 32 + i])
+                                       : 0u;
                     }
                     if (row_valid) {
 #pragma unroll
@@ -505,28 +625,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             } else if (nkt > 0) {
 #pragma unroll
-                for (int cb = 0; cb < D / 32; ++cb) {
+                for (int cb = 0; cb < HD / 32; ++cb) {
                     uint32_t v[32];
                     tmem_ld32(t_o + cb * 32, v);
                     tmem_wait_ld();
                     if (row_valid) {
-                        float4* dst = reinterpret_cast<float4*>(p.o_acc + static_cast<int64_t>(rg) * D + cb * 32);
+                        float4* dst = reinterpret_cast<float4*>(p.o_acc + static_cast<int64_t>(rg) * D + hf * HD + cb * 32);
 #pragma unroll
                         for (int i = 0; i < 8; ++i)
                             dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
                                                  __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
                     }
                 }
-                if (row_valid) {
+                if (row_valid && hf == 0) {
                     p.m_acc[rg] = m_run;
-                    p.l_acc[rg] = l_run;
+                    p.l_acc[rg] = l_tot;
                 }
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 9) {
+    if (warp == WARP_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }

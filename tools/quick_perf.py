@@ -9,7 +9,8 @@ ctxlen = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 c = int(sys.argv[3]) if len(sys.argv) > 3 else 18944
 t0 = time.time()
-hi = HeadInfer(L, 32, 8, 128, ctxlen + 128, c)
+from paper_2502_12574_b200._lib import HI_FLAG_TIMING
+hi = HeadInfer(L, 32, 8, 128, ctxlen + 128, c, flags=HI_FLAG_TIMING)
 print(f"init {time.time()-t0:.1f}s stats={hi.stats()}", flush=True)
 t0 = time.time()
 buf_k = torch.empty((c, 1, 128), dtype=torch.bfloat16, device="cuda"); buf_v = torch.empty_like(buf_k)
@@ -28,13 +29,17 @@ out = torch.empty_like(Q)
 for it in range(3):
     for l in range(L): hi.set_seq_len(l, s)
     torch.cuda.synchronize()
+    st0 = hi.stats()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for l in range(L): hi.prefill_chunk(l, Q, K, V, out)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    st1 = hi.stats()
     fl = L * 4 * 128 * 32 * (s * c + c * (c + 1) / 2)
-    print(f"prefill chunk s={s} L={L}: {ms:.1f} ms  {fl/ms/1e9:.1f} TFLOP/s  tok/s={c/ms*1e3*32/L:.0f} (32-layer equiv)", flush=True)
+    kms = st1["prefill_attn_ms"] - st0["prefill_attn_ms"]
+    kfl = st1["prefill_attn_flops"] - st0["prefill_attn_flops"]
+    print(f"prefill chunk s={s} L={L}: {ms:.1f} ms  {fl/ms/1e9:.1f} TFLOP/s  kernel {kms:.1f} ms {kfl/max(kms,1e-9)/1e9:.1f} TFLOP/s", flush=True)
 q = Q[0].contiguous(); k = K[0].contiguous(); v = V[0].contiguous(); o = torch.empty_like(q)
 for it in range(3):
     for l in range(L): hi.set_seq_len(l, ctxlen - 1)

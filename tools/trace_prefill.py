@@ -28,10 +28,10 @@ assert lib.hi_debug_prefill_trace(ctypes.c_void_p(buf.ctypes.data), ctypes.c_siz
 names = {10: "A.wait_done", 0: "A.ld_done", 1: "A.max", 2: "A.exp", 3: "A.st_done", 4: "A.arrived",
          11: "B.wait_done", 5: "B.ld_done", 6: "B.max", 7: "B.exp", 8: "B.st_done", 9: "B.arrived",
          12: "M.pA", 13: "M.issA", 14: "M.pB", 15: "M.issB"}
-t0 = int(buf[12, 100])
+t0 = int(buf[10, 100])
 print("j   " + " ".join(f"{names[k]:>11s}" for k in [10, 0, 1, 2, 3, 4, 12, 13, 11, 5, 6, 7, 8, 9, 14, 15]))
 for j in range(100, 112):
     row = [int(buf[k, j]) - t0 for k in [10, 0, 1, 2, 3, 4, 12, 13, 11, 5, 6, 7, 8, 9, 14, 15]]
     print(f"{j:3d} " + " ".join(f"{v:11d}" for v in row))
-per = (int(buf[12, 400]) - int(buf[12, 100])) / 300
+per = (int(buf[10, 400]) - int(buf[10, 100])) / 300
 print(f"period per KV tile (both Q tiles): {per:.0f} cycles; ideal TC time 2048")
