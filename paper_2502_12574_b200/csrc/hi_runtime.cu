@@ -265,8 +265,9 @@ int64_t decode_parts_for_block(int64_t nk) {
 }
 
 cudaError_t launch_prefill(hi_ctx* c, const hi::PrefillParams& p) {
-    return (c->flags & HI_FLAG_MMA_SYNC_PREFILL) ? hi::launch_prefill_mma(p, c->d, c->s_comp)
-                                                 : hi::launch_prefill_tc(p, c->d, c->s_comp);
+    if (c->flags & HI_FLAG_MMA_SYNC_PREFILL) return hi::launch_prefill_mma(p, c->d, c->s_comp);
+    if (c->d == 128 && !(c->flags & HI_FLAG_PREFILL_1CTA)) return hi::launch_prefill_tc2(p, c->d, c->s_comp);
+    return hi::launch_prefill_tc(p, c->d, c->s_comp);
 }
 
 hi_status check_call(hi_ctx* c, int layer) {
