@@ -77,8 +77,8 @@ typedef struct hi_options {
 #define HI_FLAG_TIMING 0x8       /* bracket every attention kernel launch with timing events on the
                                     compute stream; durations are summed into hi_stats at the next
                                     hi_synchronize / hi_get_stats (bench roofline evidence) */
-#define HI_FLAG_PREFILL_1CTA 0x20     /* head_dim 128: use the single-CTA tcgen05 prefill kernel instead of
-                                         the CTA-pair (cta_group::2) kernel (A/B comparisons) */
+#define HI_FLAG_PREFILL_2CTA 0x20     /* head_dim 128: use the CTA-pair (cta_group::2, M = 256) tcgen05 prefill
+                                         kernel instead of the single-CTA one (A/B comparisons; measured slower) */
 #define HI_FLAG_MMA_SYNC_PREFILL 0x10 /* run prefill attention on the legacy mma.sync kernel instead of the
                                          tcgen05/TMEM/TMA kernel (baseline comparator for benches only) */
 

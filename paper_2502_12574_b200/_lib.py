@@ -21,7 +21,7 @@ HI_FLAG_NO_HUGEPAGE = 0x2
 HI_FLAG_SERIALIZE = 0x4
 HI_FLAG_TIMING = 0x8
 HI_FLAG_MMA_SYNC_PREFILL = 0x10
-HI_FLAG_PREFILL_1CTA = 0x20
+HI_FLAG_PREFILL_2CTA = 0x20
 HI_RESIDENT_AUTO = -1
 
 # every symbol include/headinfer.h declares (checked by tests/test_abi.py)

@@ -41,8 +41,8 @@ struct PrefillParams {
     float* l_acc;             // [n_q*g]
     int flags;
 };
-// sm_100a kernels: TMA + tcgen05.mma + TMEM.  k_prefill_tc2.cu: CTA pairs (cta_group::2, M = 256),
-// head_dim 128 -- the product path; k_prefill_tc.cu: one CTA per 256 rows (any head_dim)
+// sm_100a kernels: TMA + tcgen05.mma + TMEM.  k_prefill_tc.cu: one CTA per 256 rows (any head_dim) --
+// the product path; k_prefill_tc2.cu: CTA pairs (cta_group::2, M = 256), head_dim 128, HI_FLAG_PREFILL_2CTA
 cudaError_t launch_prefill_tc2(const PrefillParams& p, int d, cudaStream_t stream);
 cudaError_t launch_prefill_tc(const PrefillParams& p, int d, cudaStream_t stream);
 // baseline comparator: mma.sync m16n8k16 (k_prefill_mma.cu), selected by HI_FLAG_MMA_SYNC_PREFILL

@@ -266,7 +266,7 @@ int64_t decode_parts_for_block(int64_t nk) {
 
 cudaError_t launch_prefill(hi_ctx* c, const hi::PrefillParams& p) {
     if (c->flags & HI_FLAG_MMA_SYNC_PREFILL) return hi::launch_prefill_mma(p, c->d, c->s_comp);
-    if (c->d == 128 && !(c->flags & HI_FLAG_PREFILL_1CTA)) return hi::launch_prefill_tc2(p, c->d, c->s_comp);
+    if (c->d == 128 && (c->flags & HI_FLAG_PREFILL_2CTA)) return hi::launch_prefill_tc2(p, c->d, c->s_comp);
     return hi::launch_prefill_tc(p, c->d, c->s_comp);
 }
 
