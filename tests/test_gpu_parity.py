@@ -161,3 +161,15 @@ def test_resident_heads_next1(resident):
     if st["resident_kv_heads"] == 8:
         assert st["host_store_bytes"] == 0 and st["h2d_bytes"] == 0
     ctx.close()
+
+
+@pytest.mark.parametrize("g", [1, 4, 8])
+def test_cta_pair_kernel(g):
+    """The CTA-pair (cta_group::2, M = 256) prefill kernel behind HI_FLAG_PREFILL_2CTA (head_dim 128)."""
+    r = Run(layers=2, q_heads=2 * g, kv_heads=2, d=128, chunks=[300, 300, 555], n_decode=2, dist="P",
+            opts=dict(slot_tokens=256, flags=0x20))
+    gpu, ctx = run_gpu(r)
+    ref, inputs = run_oracle(r)
+    compare(gpu, ref)
+    check_host_kv(ctx, r, inputs)
+    ctx.close()
