@@ -2,9 +2,11 @@
 # compute-sanitizer passes over small GPU parity cases (run under gpurun).  Writes gpurun_out/sanitize_*.log
 set -u
 CS=/usr/local/cuda/bin/compute-sanitizer
-SEL="tests/test_gpu_parity.py::test_tiny_config_end_to_end tests/test_gpu_parity.py::test_block_and_slot_geometry"
+SEL="tests/test_gpu_parity.py"
+K="tiny_config_end_to_end and P or block_and_slot_geometry and 2-64 or resident_heads_next1 and 3 or cta_pair_kernel and 4 or llama8b_shape"
+rm -f gpurun_out/sanitize_summary.txt
 for tool in memcheck racecheck synccheck; do
-  timeout 900 $CS --tool $tool --target-processes all --print-limit 20 --error-exitcode 99 \
-      python -m pytest $SEL -x -q -k "P or S or 2-64" > gpurun_out/sanitize_$tool.log 2>&1
-  echo "$tool rc=$?" >> gpurun_out/sanitize_summary.txt
+  timeout 1200 $CS --tool $tool --target-processes all --print-limit 20 --error-exitcode 99 \
+      python -m pytest $SEL -x -q -k "$K" > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$? $(grep -c 'ERROR SUMMARY: 0 errors' gpurun_out/sanitize_$tool.log) clean-summaries, $(grep -E '[0-9]+ passed' -o gpurun_out/sanitize_$tool.log | tail -1)" >> gpurun_out/sanitize_summary.txt
 done
