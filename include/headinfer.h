@@ -67,6 +67,11 @@ typedef struct hi_options {
                               (2*max_ctx*head_dim bf16 each) -- updated in place, never offloaded, attended
                               straight from HBM; the rest are offloaded as usual.  0 (default) = pure head-
                               wise offload; HI_RESIDENT_AUTO = as many pairs as fit in free HBM minus ~12 GiB */
+    int head_group;       /* NEXT-2 (§4 "adaptive head-wise offloading"; App. D; Tab. 5-7
+                              P:L513-606): kv heads moved and computed per unit (one H2D per block carries
+                              `head_group` heads; one kernel launch covers them).  Default 1 = finest
+                              head-wise offload; kv_heads/world = layer-wise offload.  Staging grows to
+                              head_group heads at max_ctx.  Must divide kv_heads/world. */
 } hi_options;
 
 #define HI_RESIDENT_AUTO (-1)
@@ -85,7 +90,7 @@ typedef struct hi_options {
 typedef struct hi_stats {
     int64_t host_store_bytes;     /* pinned host KV bytes (L * Hkv_loc * max_ctx * 4 * d) */
     int64_t staging_bytes;        /* device staging slots, total */
-    int64_t staging_bound_bytes;  /* one head at max_ctx: 4*d*max_ctx (Eq. 11, reading R8) */
+    int64_t staging_bound_bytes;  /* head_group heads at max_ctx: 4*d*max_ctx*head_group (Eq. 11, reading R8) */
     int64_t workspace_bytes;      /* other device buffers (pack, accumulators, partials) */
     int64_t h2d_bytes;            /* cumulative history bytes streamed host->device */
     int64_t d2h_bytes;            /* cumulative new-K/V bytes written back device->host */
@@ -104,6 +109,7 @@ typedef struct hi_stats {
     int64_t slot_tokens;
     int resident_kv_heads;        /* H_on pairs held in HBM (NEXT-1) */
     int64_t resident_bytes;       /* their device KV bytes */
+    int head_group;               /* kv heads per offload unit (NEXT-2) */
 } hi_stats;
 
 /*

@@ -40,6 +40,11 @@ struct PrefillParams {
     float* m_acc;             // [n_q*g]
     float* l_acc;             // [n_q*g]
     int flags;
+    // head groups (NEXT-2): n_heads kv heads per launch (blockIdx.y); head h's q/out columns start at
+    // (h*g)*d, its keys at k/v + h*kv_head_stride, its running state at + h*state_rows rows
+    int n_heads;              // 1 = one kv head (k_prefill_mma.cu / k_prefill_tc2.cu support only 1)
+    int64_t kv_head_stride;   // elements
+    int64_t state_rows;       // rows of O/m/l state per head (>= n_q*g)
 };
 // sm_100a kernels: TMA + tcgen05.mma + TMEM.  k_prefill_tc.cu: one CTA per 256 rows (any head_dim) --
 // the product path; k_prefill_tc2.cu: CTA pairs (cta_group::2, M = 256), head_dim 128, HI_FLAG_PREFILL_2CTA

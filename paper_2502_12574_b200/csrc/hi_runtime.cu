@@ -76,6 +76,7 @@ struct hi_ctx {
     int n_slots = 0;
     int64_t slot_tokens = 0;
     size_t slot_bytes = 0;
+    int group = 1;                     // NEXT-2: kv heads per transfer + kernel unit (slot holds `group` heads)
     uint8_t* d_stage = nullptr;
     std::vector<Slot> slots;
     int next_slot = 0;
@@ -86,9 +87,9 @@ struct hi_ctx {
     std::vector<cudaEvent_t> ev_kvnew_free;  // decode: kvnew[layer] read by its D2H
     // workspaces
     __nv_bfloat16* d_pack = nullptr;   // [Hkv_loc][2][chunk][d]
-    float* d_oacc = nullptr;           // [chunk*g][d]
-    float* d_macc = nullptr;           // [chunk*g]
-    float* d_lacc = nullptr;           // [chunk*g]
+    float* d_oacc = nullptr;           // [group][chunk*g][d]
+    float* d_macc = nullptr;           // [group][chunk*g]
+    float* d_lacc = nullptr;           // [group][chunk*g]
     float* d_parts = nullptr;          // [Hkv_loc][max_parts][g][d+4]
     int max_parts = 0;
     __nv_bfloat16* d_kvnew = nullptr;  // [L][2][Hkv_loc][d]
@@ -124,8 +125,10 @@ struct hi_ctx {
     // where the KV rows of (layer, h) live: device cache (resident) or host store (offloaded)
     uint8_t* kv_k(int layer, int h, int64_t row) const { return resident(layer, h) ? dev_k(layer, h, row) : host_k(layer, h, row); }
     uint8_t* kv_v(int layer, int h, int64_t row) const { return resident(layer, h) ? dev_v(layer, h, row) : host_v(layer, h, row); }
-    uint8_t* slot_k(int s) const { return d_stage + static_cast<size_t>(s) * slot_bytes; }
-    uint8_t* slot_v(int s) const { return slot_k(s) + static_cast<size_t>(slot_tokens) * d * 2; }
+    // slot s holds `group` heads, each [K: slot_tokens x d | V: slot_tokens x d]
+    size_t slot_head_bytes() const { return static_cast<size_t>(slot_tokens) * d * 2 * 2; }
+    uint8_t* slot_k(int s, int gh = 0) const { return d_stage + static_cast<size_t>(s) * slot_bytes + gh * slot_head_bytes(); }
+    uint8_t* slot_v(int s, int gh = 0) const { return slot_k(s, gh) + static_cast<size_t>(slot_tokens) * d * 2; }
 };
 
 namespace {
@@ -265,9 +268,23 @@ int64_t decode_parts_for_block(int64_t nk) {
 }
 
 cudaError_t launch_prefill(hi_ctx* c, const hi::PrefillParams& p) {
-    if (c->flags & HI_FLAG_MMA_SYNC_PREFILL) return hi::launch_prefill_mma(p, c->d, c->s_comp);
-    if (c->d == 128 && (c->flags & HI_FLAG_PREFILL_2CTA)) return hi::launch_prefill_tc2(p, c->d, c->s_comp);
-    return hi::launch_prefill_tc(p, c->d, c->s_comp);
+    const bool mma = c->flags & HI_FLAG_MMA_SYNC_PREFILL;
+    const bool pair = !mma && c->d == 128 && (c->flags & HI_FLAG_PREFILL_2CTA);
+    if (!mma && !pair) return hi::launch_prefill_tc(p, c->d, c->s_comp);  // head groups in one launch (grid.y)
+    for (int h = 0; h < std::max(1, p.n_heads); ++h) {  // single-head kernels: one launch per head of the group
+        hi::PrefillParams q1 = p;
+        q1.n_heads = 1;
+        q1.q = p.q + static_cast<int64_t>(h) * p.g * c->d;
+        q1.out = p.out + static_cast<int64_t>(h) * p.g * c->d;
+        q1.k = p.k + h * p.kv_head_stride;
+        q1.v = p.v + h * p.kv_head_stride;
+        q1.o_acc = p.o_acc + h * p.state_rows * c->d;
+        q1.m_acc = p.m_acc + h * p.state_rows;
+        q1.l_acc = p.l_acc + h * p.state_rows;
+        const cudaError_t e = mma ? hi::launch_prefill_mma(q1, c->d, c->s_comp) : hi::launch_prefill_tc2(q1, c->d, c->s_comp);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 hi_status check_call(hi_ctx* c, int layer) {
@@ -277,9 +294,9 @@ hi_status check_call(hi_ctx* c, int layer) {
     return HI_OK;
 }
 
-// Enqueue the H2D of history block [k0, k0+nk) of (layer, h) into the next slot; the compute
-// stream is made to wait for it.  Returns the slot index through *slot_out.
-hi_status stage_block(hi_ctx* c, int layer, int h, int64_t k0, int64_t nk, int* slot_out) {
+// Enqueue the H2D of history block [k0, k0+nk) of kv heads [h0, h0+nh) of `layer` into the next slot;
+// the compute stream is made to wait for it.  Returns the slot index through *slot_out.
+hi_status stage_block(hi_ctx* c, int layer, int h0, int nh, int64_t k0, int64_t nk, int* slot_out) {
     const int s = c->next_slot;
     c->next_slot = (c->next_slot + 1) % c->n_slots;
     Slot& sl = c->slots[s];
@@ -289,11 +306,13 @@ hi_status stage_block(hi_ctx* c, int layer, int h, int64_t k0, int64_t nk, int* 
         ++c->launches;
     }
     const size_t bytes = static_cast<size_t>(nk) * c->d * 2;
-    HI_CK(c, cudaMemcpyAsync(c->slot_k(s), c->host_k(layer, h, k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
-    HI_CK(c, cudaMemcpyAsync(c->slot_v(s), c->host_v(layer, h, k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
+    for (int gh = 0; gh < nh; ++gh) {
+        HI_CK(c, cudaMemcpyAsync(c->slot_k(s, gh), c->host_k(layer, h0 + gh, k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
+        HI_CK(c, cudaMemcpyAsync(c->slot_v(s, gh), c->host_v(layer, h0 + gh, k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
+    }
     HI_CK(c, cudaEventRecord(sl.ready, c->s_h2d));
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, sl.ready, 0));  // RAW: block landed
-    c->h2d_bytes += static_cast<int64_t>(2 * bytes);
+    c->h2d_bytes += static_cast<int64_t>(2 * bytes) * nh;
     *slot_out = s;
     return HI_OK;
 }
@@ -398,8 +417,11 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     hi_options o{};
     if (opt) o = *opt;
     if (o.n_slots == 0) o.n_slots = 4;
-    if (o.n_slots < 2 || o.n_slots > 64 || o.slot_tokens < 0 || o.resident_kv_heads < HI_RESIDENT_AUTO) {
-        g_init_error = "invalid hi_options (n_slots in [2,64], slot_tokens >= 0, resident_kv_heads >= -1)";
+    if (o.head_group == 0) o.head_group = 1;
+    if (o.n_slots < 2 || o.n_slots > 64 || o.slot_tokens < 0 || o.resident_kv_heads < HI_RESIDENT_AUTO ||
+        o.head_group < 1 || (kv_heads / world) % o.head_group != 0) {
+        g_init_error = "invalid hi_options (n_slots in [2,64], slot_tokens >= 0, resident_kv_heads >= -1, "
+                       "head_group >= 1 dividing kv_heads/world)";
         return HI_EINVAL;
     }
 
@@ -413,7 +435,8 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     int64_t st = o.slot_tokens;
     if (st == 0) st = std::max<int64_t>(64, (max_ctx / o.n_slots) / 64 * 64);
     c->slot_tokens = st;
-    c->slot_bytes = static_cast<size_t>(st) * head_dim * 2 * 2;
+    c->group = o.head_group;
+    c->slot_bytes = static_cast<size_t>(st) * head_dim * 2 * 2 * c->group;
 
     auto bail = [&](hi_status s, const std::string& msg) {
         g_init_error = msg.empty() ? c->err : msg;
@@ -466,7 +489,7 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     c->max_parts = static_cast<int>(std::max<int64_t>(max_blocks * decode_parts_for_block(std::min<int64_t>(st, max_ctx)),
                                                      decode_parts_for_block(max_ctx)) + 8);
     const size_t pack_b = static_cast<size_t>(c->Hkv_loc) * 2 * chunk * head_dim * 2;
-    const size_t oacc_b = rows * head_dim * 4, ml_b = rows * 4;
+    const size_t oacc_b = rows * head_dim * 4 * c->group, ml_b = rows * 4 * c->group;
     const size_t parts_b = static_cast<size_t>(c->Hkv_loc) * c->max_parts * g * (head_dim + 4) * 4;
     const size_t kvnew_b = static_cast<size_t>(layers) * 2 * c->Hkv_loc * head_dim * 2;
     if (!dmalloc(reinterpret_cast<void**>(&c->d_pack), pack_b) || !dmalloc(reinterpret_cast<void**>(&c->d_oacc), oacc_b) ||
@@ -555,10 +578,13 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     p.o_acc = c->d_oacc;
     p.m_acc = c->d_macc;
     p.l_acc = c->d_lacc;
-    for (int h = 0; h < Hkv; ++h) {
+    p.state_rows = static_cast<int64_t>(c->chunk) * g;
+    const int r_l = c->resident_heads_of_layer(layer);
+    // H_on heads of this layer (NEXT-1): chunk segment + the whole history straight from the HBM cache
+    for (int h = 0; h < r_l; ++h) {
+        p.n_heads = 1;
         p.q = static_cast<const __nv_bfloat16*>(Q) + static_cast<size_t>(h) * g * d;
         p.out = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(h) * g * d;
-        // the chunk's own keys first: causal, no transfer needed
         p.k = c->d_pack + (static_cast<size_t>(h) * 2 + 0) * n * d;
         p.v = c->d_pack + (static_cast<size_t>(h) * 2 + 1) * n * d;
         p.kv_row_stride = d;
@@ -571,36 +597,55 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
             tm.done(4.0 * d * g * (static_cast<double>(n) * (n + 1) / 2.0), true);
         }
         ++c->launches;
-        if (c->resident(layer, h)) {  // H_on: the whole history [0, s) straight from the HBM cache
-            if (s > 0) {
-                p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, h, 0));
-                p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, h, 0));
-                p.n_k = static_cast<int>(s);
-                p.k_pos0 = 0;
-                p.flags = hi::PF_LAST;
-                LaunchTimer tm(c);
-                HI_CK(c, launch_prefill(c, p));
-                tm.done(4.0 * d * g * static_cast<double>(n) * static_cast<double>(s), true);
-                ++c->launches;
-            }
-            continue;
+        if (s > 0) {
+            p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, h, 0));
+            p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, h, 0));
+            p.n_k = static_cast<int>(s);
+            p.k_pos0 = 0;
+            p.flags = hi::PF_LAST;
+            LaunchTimer tm(c);
+            HI_CK(c, launch_prefill(c, p));
+            tm.done(4.0 * d * g * static_cast<double>(n) * static_cast<double>(s), true);
+            ++c->launches;
         }
-        // history blocks [0, s) through the staging slots (Alg. 1 line 10 prefetch)
+    }
+    // offloaded heads, `group` at a time (Alg. 1 line 5 loop; NEXT-2 head groups when group > 1)
+    for (int h0 = r_l; h0 < Hkv; h0 += c->group) {
+        const int nh = std::min(c->group, Hkv - h0);
+        p.n_heads = nh;
+        p.q = static_cast<const __nv_bfloat16*>(Q) + static_cast<size_t>(h0) * g * d;
+        p.out = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(h0) * g * d;
+        // the chunk's own keys first: causal, no transfer needed (pack buffer: [h][K|V][n][d])
+        p.k = c->d_pack + (static_cast<size_t>(h0) * 2 + 0) * n * d;
+        p.v = c->d_pack + (static_cast<size_t>(h0) * 2 + 1) * n * d;
+        p.kv_row_stride = d;
+        p.kv_head_stride = static_cast<int64_t>(2) * n * d;
+        p.n_k = n;
+        p.k_pos0 = s;
+        p.flags = hi::PF_FIRST | hi::PF_CAUSAL | (s == 0 ? hi::PF_LAST : 0);
+        {
+            LaunchTimer tm(c);
+            HI_CK(c, launch_prefill(c, p));
+            tm.done(4.0 * d * g * nh * (static_cast<double>(n) * (n + 1) / 2.0), true);
+        }
+        ++c->launches;
+        // history blocks [0, s) of the group's heads through the staging slots (Alg. 1 line 10 prefetch)
         for (int64_t b = 0; b < nb; ++b) {
             const int64_t k0 = b * c->slot_tokens;
             const int64_t nk = std::min<int64_t>(c->slot_tokens, s - k0);
             int slot = 0;
-            st = stage_block(c, layer, h, k0, nk, &slot);
+            st = stage_block(c, layer, h0, nh, k0, nk, &slot);
             if (st != HI_OK) return st;
             p.k = reinterpret_cast<const __nv_bfloat16*>(c->slot_k(slot));
             p.v = reinterpret_cast<const __nv_bfloat16*>(c->slot_v(slot));
+            p.kv_head_stride = static_cast<int64_t>(c->slot_head_bytes() / 2);
             p.n_k = static_cast<int>(nk);
             p.k_pos0 = k0;
             p.flags = (b == nb - 1) ? hi::PF_LAST : 0;
             {
                 LaunchTimer tm(c);
                 HI_CK(c, launch_prefill(c, p));
-                tm.done(4.0 * d * g * static_cast<double>(n) * static_cast<double>(nk), true);
+                tm.done(4.0 * d * g * nh * static_cast<double>(n) * static_cast<double>(nk), true);
             }
             ++c->launches;
             st = release_slot(c, slot);
@@ -675,27 +720,31 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
         tm.done(4.0 * d * static_cast<double>(s) * r_l, false);
         ++c->launches;
     }
-    for (int h = r_l; h < Hkv; ++h) {
+    for (int h0 = r_l; h0 < Hkv; h0 += c->group) {
+        const int nh = std::min(c->group, Hkv - h0);
         int pofs = 0;
         for (int64_t b = 0; b < nb; ++b) {
             const int64_t k0 = b * c->slot_tokens;
             const int64_t nk = std::min<int64_t>(c->slot_tokens, s - k0);
             int slot = 0;
-            st = stage_block(c, layer, h, k0, nk, &slot);
+            st = stage_block(c, layer, h0, nh, k0, nk, &slot);
             if (st != HI_OK) return st;
             hi::DecodePartialParams p{};
-            p.q = static_cast<const __nv_bfloat16*>(q) + static_cast<size_t>(h) * g * d;
+            p.q = static_cast<const __nv_bfloat16*>(q) + static_cast<size_t>(h0) * g * d;
             p.k = reinterpret_cast<const __nv_bfloat16*>(c->slot_k(slot));
             p.v = reinterpret_cast<const __nv_bfloat16*>(c->slot_v(slot));
             p.n_k = static_cast<int>(nk);
-            p.split_len = decode_split_len(nk);
+            p.split_len = decode_split_len(nk, nh);
             p.scale_log2 = c->scale_log2;
-            p.parts = c->d_parts + (static_cast<size_t>(h) * c->max_parts + pofs) * g * (d + 4);
+            p.parts = c->d_parts + (static_cast<size_t>(h0) * c->max_parts + pofs) * g * (d + 4);
+            p.kv_head_stride = static_cast<int64_t>(c->slot_head_bytes() / 2);
+            p.q_head_stride = static_cast<int64_t>(g) * d;
+            p.parts_head_stride = static_cast<int64_t>(c->max_parts) * g * (d + 4);
             const int nsp = static_cast<int>((nk + p.split_len - 1) / p.split_len);
             {
                 LaunchTimer tm(c);
-                HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, 1, c->s_comp));
-                tm.done(4.0 * d * static_cast<double>(nk), false);
+                HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, nh, c->s_comp));
+                tm.done(4.0 * d * static_cast<double>(nk) * nh, false);
             }
             ++c->launches;
             pofs += nsp;
@@ -803,7 +852,7 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     memset(o, 0, sizeof *o);
     o->host_store_bytes = static_cast<int64_t>(c->host_bytes);
     o->staging_bytes = static_cast<int64_t>(c->slot_bytes) * c->n_slots;
-    o->staging_bound_bytes = 4ll * c->d * c->max_ctx;
+    o->staging_bound_bytes = 4ll * c->d * c->max_ctx * c->group;  // `group` heads at max_ctx (one head: group 1)
     o->workspace_bytes = static_cast<int64_t>(c->workspace_bytes);
     o->h2d_bytes = c->h2d_bytes;
     o->d2h_bytes = c->d2h_bytes;
@@ -819,6 +868,7 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     o->init_seconds = c->init_seconds;
     o->resident_kv_heads = c->n_res;
     o->resident_bytes = static_cast<int64_t>(c->res_bytes);
+    o->head_group = c->group;
     o->numa_node = c->numa_node;
     o->n_slots = c->n_slots;
     o->slot_tokens = c->slot_tokens;

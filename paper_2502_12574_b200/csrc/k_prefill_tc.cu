@@ -134,6 +134,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int g = p.g;
     const int n_rows = p.n_q * g;
     const int row0 = blockIdx.x * (2 * BM);
+    const int hh = blockIdx.y;                 // kv head within the launch's head group
+    float* const o_acc = p.o_acc + static_cast<int64_t>(hh) * p.state_rows * D;
+    float* const m_acc = p.m_acc + static_cast<int64_t>(hh) * p.state_rows;
+    float* const l_acc = p.l_acc + static_cast<int64_t>(hh) * p.state_rows;
     const bool first = p.flags & PF_FIRST, last = p.flags & PF_LAST, causal = p.flags & PF_CAUSAL;
     const int n_tiles = (row0 + BM < n_rows) ? 2 : 1;  // second Q tile may be empty at the tail
 
@@ -192,17 +196,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_expect_tx(bar_q, n_tiles * (D / 64) * L::BOX);
             for (int tt = 0; tt < n_tiles; ++tt)
                 for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sbase + L::Q_OFF + (tt * (D / 64) + c) * L::BOX, &tm_q, bar_q, c * 64, 0,
+                    tma_load_3d(sbase + L::Q_OFF + (tt * (D / 64) + c) * L::BOX, &tm_q, bar_q, c * 64, hh * g,
                                 (row0 + tt * BM) / g);
             for (int i = 0; i < n_kt; ++i) {
                 const int s = i % NS;
                 if (i >= NS) mbar_wait(bar_e(s), ((i / NS) - 1) & 1);
                 mbar_expect_tx(bar_k(s), (D / 64) * L::BOX);
                 for (int c = 0; c < D / 64; ++c)
-                    tma_load_2d(sbase + L::K_OFF + (s * (D / 64) + c) * L::BOX, &tm_k, bar_k(s), c * 64, i * BN);
+                    tma_load_3d(sbase + L::K_OFF + (s * (D / 64) + c) * L::BOX, &tm_k, bar_k(s), c * 64, i * BN, hh);
                 mbar_expect_tx(bar_v(s), (D / 64) * L::BOX);
                 for (int c = 0; c < D / 64; ++c)
-                    tma_load_2d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, i * BN);
+                    tma_load_3d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, i * BN, hh);
             }
         } else if (warp == WARP_MMA && lane == 0 && n_kt > 0) {
             // ============================ MMA issuer ==============================
@@ -289,14 +293,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float m_run = -CUDART_INF_F, l_run = 0.f;  // l_run: this thread's partial row sum
         if (tt < n_tiles) {
             if (!first) {
-                m_run = row_valid ? p.m_acc[rg] : -CUDART_INF_F;
-                l_run = (row_valid && hf == 0) ? p.l_acc[rg] : 0.f;
+                m_run = row_valid ? m_acc[rg] : -CUDART_INF_F;
+                l_run = (row_valid && hf == 0) ? l_acc[rg] : 0.f;
                 if (nkt > 0) {  // running O -> TMEM before the first PV accumulates onto it
 #pragma unroll
                     for (int cb = 0; cb < HD / 32; ++cb) {
                         uint32_t v[32];
                         const float4* src = reinterpret_cast<const float4*>(
-                            p.o_acc + static_cast<int64_t>(row_valid ? rg : 0) * D + hf * HD + cb * 32);
+                            o_acc + static_cast<int64_t>(row_valid ? rg : 0) * D + hf * HD + cb * 32);
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
                             float4 f = row_valid ? src[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (last) {
                 const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
-                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (rg % g) * D + hf * HD;
+                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (hh * g + rg % g) * D + hf * HD;
 #pragma unroll
                 for (int cb = 0; cb < HD / 32; ++cb) {
                     uint32_t v[32];
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
                             v[i] = (row_valid && !first)
-                                       ? __float_as_uint(p.o_acc[static_cast<int64_t>(rg) * D + hf * HD + cb * 32 + i])
+                                       ? __float_as_uint(o_acc[static_cast<int64_t>(rg) * D + hf * HD + cb * 32 + i])
                                        : 0u;
                     }
                     if (row_valid) {
@@ -485,7 +489,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tmem_ld32(t_o + cb * 32, v);
                     tmem_wait_ld();
                     if (row_valid) {
-                        float4* dst = reinterpret_cast<float4*>(p.o_acc + static_cast<int64_t>(rg) * D + hf * HD + cb * 32);
+                        float4* dst = reinterpret_cast<float4*>(o_acc + static_cast<int64_t>(rg) * D + hf * HD + cb * 32);
 #pragma unroll
                         for (int i = 0; i < 8; ++i)
                             dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
@@ -493,8 +497,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
                 if (row_valid && hf == 0) {
-                    p.m_acc[rg] = m_run;
-                    p.l_acc[rg] = l_tot;
+                    m_acc[rg] = m_run;
+                    l_acc[rg] = l_tot;
                 }
             }
         }
@@ -512,6 +516,7 @@ template <int D>
 cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
     const int n_rows = p.n_q * p.g;
     const int grid = (n_rows + 2 * BM - 1) / (2 * BM);
+    const int heads = p.n_heads > 0 ? p.n_heads : 1;
     if (grid == 0) return cudaSuccess;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -521,19 +526,23 @@ cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
     if (attr_err != cudaSuccess) return attr_err;
     CUtensorMap tq, tk, tv;
     {
-        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.g), static_cast<cuuint64_t>(p.n_q)};
+        // (d, q heads of the launch's head group, tokens): head h's g rows start at coordinate h*g
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.g) * heads,
+                                    static_cast<cuuint64_t>(p.n_q)};
         const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(p.q_tok_stride) * 2};
         const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(p.g), static_cast<cuuint32_t>(BM / p.g)};
         if (!make_tmap_bf16(&tq, p.q, 3, dims, strides, box)) return cudaErrorInvalidValue;
     }
     {
-        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k)};
-        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.kv_row_stride) * 2};
-        const cuuint32_t box[2] = {64, BN};
-        if (!make_tmap_bf16(&tk, p.k, 2, dims, strides, box)) return cudaErrorInvalidValue;
-        if (!make_tmap_bf16(&tv, p.v, 2, dims, strides, box)) return cudaErrorInvalidValue;
+        // (d, keys, kv heads of the group)
+        const int64_t hs = heads > 1 ? p.kv_head_stride : static_cast<int64_t>(p.n_k) * p.kv_row_stride;
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k), static_cast<cuuint64_t>(heads)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.kv_row_stride) * 2, static_cast<cuuint64_t>(hs) * 2};
+        const cuuint32_t box[3] = {64, BN, 1};
+        if (!make_tmap_bf16(&tk, p.k, 3, dims, strides, box)) return cudaErrorInvalidValue;
+        if (!make_tmap_bf16(&tv, p.v, 3, dims, strides, box)) return cudaErrorInvalidValue;
     }
-    prefill_tc_kernel<D><<<grid, NUM_THREADS, Smem<D>::ALLOC, stream>>>(tq, tk, tv, p);
+    prefill_tc_kernel<D><<<dim3(grid, heads), NUM_THREADS, Smem<D>::ALLOC, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();
 }
 

@@ -74,3 +74,15 @@ def test_init_without_gpu_fails_loudly(lib):
     assert lib.hi_init(1, 4, 2, 64, 1024, 256, 0, 1, ctypes.byref(h)) == 6  # HI_ECUDA, no CPU fallback
     assert not h.value
     assert b"CUDA" in lib.hi_last_error(None) or b"device" in lib.hi_last_error(None)
+
+
+@pytest.mark.parametrize("opts", [dict(head_group=3), dict(head_group=-1), dict(n_slots=1),
+                                  dict(resident_kv_heads=-2)])
+def test_init_rejects_invalid_options(lib, opts):
+    """hi_init_ex validates hi_options before touching CUDA (head_group must divide kv_heads/world)."""
+    from paper_2502_12574_b200._lib import hi_options
+    h = ctypes.c_void_p()
+    o = hi_options(**opts)
+    assert lib.hi_init_ex(1, 8, 4, 64, 1024, 256, 0, 1, ctypes.byref(o), ctypes.byref(h)) == 1
+    assert not h.value
+    assert b"hi_options" in lib.hi_last_error(None)

@@ -173,3 +173,35 @@ def test_cta_pair_kernel(g):
     compare(gpu, ref)
     check_host_kv(ctx, r, inputs)
     ctx.close()
+
+
+@pytest.mark.parametrize("group,resident,flags", [(2, 0, 0), (4, 0, 0), (8, 0, 0), (2, 3, 0), (4, 0, 0x10),
+                                                  (2, 0, 0x20)])
+def test_head_groups_next2(group, resident, flags):
+    """NEXT-2 (§4 adaptive head-wise offloading, Tab. 5-7): `group` kv heads per H2D block and per
+    kernel launch; results and host KV must not depend on the group size, with resident heads in front
+    (the groups start after them) and with the single-head kernels (mma.sync 0x10, CTA pair 0x20)."""
+    r = Run(layers=2, q_heads=16, kv_heads=8, d=128, chunks=[300, 300, 100], n_decode=4, dist="P",
+            opts=dict(slot_tokens=128, head_group=group, resident_kv_heads=resident, flags=flags))
+    gpu, ctx = run_gpu(r)
+    ref, inputs = run_oracle(r)
+    compare(gpu, ref)
+    check_host_kv(ctx, r, inputs)
+    st = ctx.stats()
+    assert st["head_group"] == group
+    assert st["staging_bytes"] <= st["staging_bound_bytes"]
+    ctx.close()
+
+
+def test_head_groups_bit_identical_to_group1():
+    """The per-head prefill arithmetic does not change with the grouping: prefill rows are bit-identical
+    for G = 1, 4 (decode rows may differ in the last bits: the split-K partition depends on how many heads
+    share a launch)."""
+    outs = []
+    for group in (1, 4):
+        r = Run(layers=1, q_heads=32, kv_heads=8, d=128, chunks=[256, 256, 77], n_decode=3, dist="U",
+                opts=dict(slot_tokens=192, head_group=group))
+        gpu, ctx = run_gpu(r)
+        outs.append(gpu[0][:589])
+        ctx.close()
+    assert torch.equal(outs[0], outs[1])

@@ -10,7 +10,8 @@ L = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 c = int(sys.argv[3]) if len(sys.argv) > 3 else 18944
 t0 = time.time()
 from paper_2502_12574_b200._lib import HI_FLAG_TIMING
-hi = HeadInfer(L, 32, 8, 128, ctxlen + 128, c, flags=HI_FLAG_TIMING | int(os.environ.get("HI_QP_FLAGS", "0"), 0))
+hi = HeadInfer(L, 32, 8, 128, ctxlen + 128, c, flags=HI_FLAG_TIMING | int(os.environ.get("HI_QP_FLAGS", "0"), 0),
+               head_group=int(os.environ.get("HI_QP_GROUP", "1")))
 print(f"init {time.time()-t0:.1f}s stats={hi.stats()}", flush=True)
 t0 = time.time()
 buf_k = torch.empty((c, 1, 128), dtype=torch.bfloat16, device="cuda"); buf_v = torch.empty_like(buf_k)
