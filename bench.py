@@ -181,7 +181,8 @@ def run_ours(args, rank, world, local_rank, pg):
         pair_b = 4 * d * max_ctx
         resident = int(max(0, min(L * hkv_loc, (free_b - inputs_b - (10 << 30)) // pair_b)))
     t0 = time.time()
-    hi = HeadInfer(L, hq, hkv, d, max_ctx, c, rank, world, flags=HI_FLAG_TIMING, resident_kv_heads=resident)
+    hi = HeadInfer(L, hq, hkv, d, max_ctx, c, rank, world, flags=HI_FLAG_TIMING, resident_kv_heads=resident,
+                   head_group=args.head_group)
     init_s = time.time() - t0
     t0 = time.time()
     fill_history(hi, L, hkv_loc, kv0h, d, s0, torch, fill_)
@@ -360,7 +361,8 @@ def run_ours(args, rank, world, local_rank, pg):
         "data": "synthetic (seeded counter-hash generator, distribution U; Llama-3-8B attention shapes, "
                 "no weights: attention-only path)",
         "config": {"workload": wl, "layers": L, "q_heads": hq, "kv_heads": hkv, "head_dim": d, "context": S,
-                   "chunk": c, "parallelism": f"head-shard{world}", "prefill_step": "1 chunk x all layers",
+                   "chunk": c, "head_group": st1["head_group"], "resident_kv_heads": R,
+                   "parallelism": f"head-shard{world}", "prefill_step": "1 chunk x all layers",
                    "timed_chunk_positions": [s0 + W * c, last_chunk_pos],
                    "decode_step": "1 token x all layers", "decode_context": [S + W, S + W + K - 1],
                    "l2": "inputs per step > L2 (>= 6 GiB), no flush needed"},
@@ -383,7 +385,8 @@ def run_ours(args, rank, world, local_rank, pg):
                      "peak_source": peaks["source"] + " bf16_tflops_sustained"},
         "clocks": clk,
         "gpu_launches": launches,
-        "residency": {"staging_bytes": st1["staging_bytes"], "one_head_bytes": st1["staging_bound_bytes"],
+        "residency": {"staging_bytes": st1["staging_bytes"], "staging_bound_bytes": st1["staging_bound_bytes"],
+                      "head_group": st1["head_group"],
                       "host_store_bytes": st1["host_store_bytes"], "init_s": round(init_s, 2),
                       "resident_kv_heads": st1["resident_kv_heads"], "resident_bytes": st1["resident_bytes"]},
     }
@@ -559,6 +562,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--resident-heads", type=int, default=0,
                     help="NEXT-1: keep the first R (layer, kv head) pairs' KV in HBM (-1 = as many as fit)")
+    ap.add_argument("--head-group", type=int, default=-1,
+                    help="NEXT-2: kv heads per transfer/launch unit (-1 = auto: >= 8 waves per chunk launch)")
     ap.add_argument("--ranks-share-gpu", action="store_true",
                     help="validation only: every rank uses cuda:0 and the output gather goes through gloo")
     args = ap.parse_args()

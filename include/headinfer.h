@@ -71,10 +71,13 @@ typedef struct hi_options {
                               P:L513-606): kv heads moved and computed per unit (one H2D per block carries
                               `head_group` heads; one kernel launch covers them).  Default 1 = finest
                               head-wise offload; kv_heads/world = layer-wise offload.  Staging grows to
-                              head_group heads at max_ctx.  Must divide kv_heads/world. */
+                              head_group heads at max_ctx.  Must divide kv_heads/world, or be
+                              HI_GROUP_AUTO (-1): the smallest divisor whose chunk launch fills
+                              >= 8 waves of 128-row tiles, staging capped at 1/32 of HBM. */
 } hi_options;
 
 #define HI_RESIDENT_AUTO (-1)
+#define HI_GROUP_AUTO (-1)
 
 #define HI_FLAG_POISON_SLOTS 0x1 /* fill each staging slot with NaN before every H2D (race detection) */
 #define HI_FLAG_NO_HUGEPAGE 0x2  /* do not madvise(MADV_HUGEPAGE) the host store */
@@ -84,6 +87,7 @@ typedef struct hi_options {
                                     hi_synchronize / hi_get_stats (bench roofline evidence) */
 #define HI_FLAG_PREFILL_2CTA 0x20     /* head_dim 128: use the CTA-pair (cta_group::2, M = 256) tcgen05 prefill
                                          kernel instead of the single-CTA one (A/B comparisons; measured slower) */
+#define HI_FLAG_PREFILL_TC1 0x40      /* use the one-tile / three-S-buffer tcgen05 prefill kernel (k_prefill_tc1.cu) */
 #define HI_FLAG_MMA_SYNC_PREFILL 0x10 /* run prefill attention on the legacy mma.sync kernel instead of the
                                          tcgen05/TMEM/TMA kernel (baseline comparator for benches only) */
 

@@ -22,7 +22,9 @@ HI_FLAG_SERIALIZE = 0x4
 HI_FLAG_TIMING = 0x8
 HI_FLAG_MMA_SYNC_PREFILL = 0x10
 HI_FLAG_PREFILL_2CTA = 0x20
+HI_FLAG_PREFILL_TC1 = 0x40
 HI_RESIDENT_AUTO = -1
+HI_GROUP_AUTO = -1
 
 # every symbol include/headinfer.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",

@@ -270,7 +270,10 @@ int64_t decode_parts_for_block(int64_t nk) {
 cudaError_t launch_prefill(hi_ctx* c, const hi::PrefillParams& p) {
     const bool mma = c->flags & HI_FLAG_MMA_SYNC_PREFILL;
     const bool pair = !mma && c->d == 128 && (c->flags & HI_FLAG_PREFILL_2CTA);
-    if (!mma && !pair) return hi::launch_prefill_tc(p, c->d, c->s_comp);  // head groups in one launch (grid.y)
+    if (!mma && !pair) {  // head groups in one launch (grid.y)
+        if (c->flags & HI_FLAG_PREFILL_TC1) return hi::launch_prefill_tc1(p, c->d, c->s_comp);
+        return hi::launch_prefill_tc(p, c->d, c->s_comp);
+    }
     for (int h = 0; h < std::max(1, p.n_heads); ++h) {  // single-head kernels: one launch per head of the group
         hi::PrefillParams q1 = p;
         q1.n_heads = 1;
@@ -419,9 +422,9 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     if (o.n_slots == 0) o.n_slots = 4;
     if (o.head_group == 0) o.head_group = 1;
     if (o.n_slots < 2 || o.n_slots > 64 || o.slot_tokens < 0 || o.resident_kv_heads < HI_RESIDENT_AUTO ||
-        o.head_group < 1 || (kv_heads / world) % o.head_group != 0) {
+        (o.head_group != HI_GROUP_AUTO && (o.head_group < 1 || (kv_heads / world) % o.head_group != 0))) {
         g_init_error = "invalid hi_options (n_slots in [2,64], slot_tokens >= 0, resident_kv_heads >= -1, "
-                       "head_group >= 1 dividing kv_heads/world)";
+                       "head_group = -1 or >= 1 dividing kv_heads/world)";
         return HI_EINVAL;
     }
 
@@ -435,8 +438,6 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     int64_t st = o.slot_tokens;
     if (st == 0) st = std::max<int64_t>(64, (max_ctx / o.n_slots) / 64 * 64);
     c->slot_tokens = st;
-    c->group = o.head_group;
-    c->slot_bytes = static_cast<size_t>(st) * head_dim * 2 * 2 * c->group;
 
     auto bail = [&](hi_status s, const std::string& msg) {
         g_init_error = msg.empty() ? c->err : msg;
@@ -452,9 +453,29 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     if (opt && opt->device >= 0 && opt->device < ndev && opt->device != 0) c->device = opt->device;
     else if (cudaGetDevice(&c->device) != cudaSuccess) c->device = 0;
     if ((e = cudaSetDevice(c->device)) != cudaSuccess) return bail(HI_ECUDA, cudaGetErrorString(e));
-    cudaDeviceProp prop;
+    cudaDeviceProp prop{};
     if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess && prop.major < 10)
         return bail(HI_ECUDA, "libheadinfer is built for sm_100a (B200); device compute capability < 10");
+
+    // head groups (NEXT-2).  Auto: the smallest divisor G of Hkv_loc whose chunk-segment launch has >= 8
+    // waves of 128-row tiles (launch fill/drain amortised, Tab. 5-7 short-context regime), while the
+    // staging ring stays <= 1/32 of device memory (the adaptive memory/speed trade-off of App. D).
+    const size_t head_slot_bytes = static_cast<size_t>(st) * head_dim * 2 * 2;
+    if (o.head_group == HI_GROUP_AUTO) {
+        const int64_t tiles = (static_cast<int64_t>(chunk) * g + 127) / 128;
+        const int sms = prop.multiProcessorCount > 0 ? prop.multiProcessorCount : 148;
+        const size_t mem_cap = prop.totalGlobalMem / 32;
+        int G = 1;
+        for (int cand = 1; cand <= c->Hkv_loc; ++cand) {
+            if (c->Hkv_loc % cand) continue;
+            if (cand > 1 && head_slot_bytes * cand * c->n_slots > mem_cap) break;
+            G = cand;
+            if (tiles * cand >= 8LL * sms) break;
+        }
+        o.head_group = G;
+    }
+    c->group = o.head_group;
+    c->slot_bytes = head_slot_bytes * c->group;
 
     // (a) residency (NEXT-1, Alg. 1 H_on): the first n_res (layer, kv head) pairs keep their KV in HBM
     const int n_pairs = layers * c->Hkv_loc;

@@ -84,6 +84,13 @@ __device__ unsigned long long g_hi_trace[16][512];
 #define HI_EX2_POLY_EVERY 1000000  // off: MUFU + polynomial measured slower (profiles/ab_prefill_r01.txt)
 #endif
 constexpr int EX2_POLY_EVERY = HI_EX2_POLY_EVERY;  // 2 of every 16 exponentials on the FMA pipe (see ex2_poly)
+// Packed softmax (sm_100 FFMA2/FADD2): of every 4 element pairs, POLY_PAIRS go through the packed
+// FMA-pipe polynomial (ex2_poly2), the rest through MUFU; -1 = the scalar loop.  Measured (131K probe,
+// profiles/ab_prefill_r01.txt): packed 0 +1.3% over scalar; 1 and 2 polynomial pairs slower.
+#ifndef HI_POLY_PAIRS
+#define HI_POLY_PAIRS 0
+#endif
+constexpr int POLY_PAIRS = HI_POLY_PAIRS;
 
 using namespace ptx;
 
@@ -408,14 +415,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const float neg_m = (m_ref == -CUDART_INF_F) ? 0.f : -m_ref;
                 // p = 2^(x*scale - m): packed to bf16 pairs in place (x[i/2] is dead once read).  Two
                 // elements in EX2_POLY_EVERY go through the FMA-pipe polynomial, the rest through MUFU.
+                if constexpr (POLY_PAIRS >= 0) {
+                    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+                    const f2 sc2{sc, sc}, nm2{neg_m, neg_m};
 #pragma unroll
-                for (int i = 0; i < HN; i += 2) {
-                    const float a0 = fmaf(__uint_as_float(x[i]), sc, neg_m);
-                    const float a1 = fmaf(__uint_as_float(x[i + 1]), sc, neg_m);
-                    const float p0 = ((i % EX2_POLY_EVERY) == EX2_POLY_EVERY - 2) ? ex2_poly(a0) : ex2(a0);
-                    const float p1 = (((i + 1) % EX2_POLY_EVERY) == EX2_POLY_EVERY - 1) ? ex2_poly(a1) : ex2(a1);
-                    ls[(i >> 1) & 3] += p0 + p1;
-                    x[i / 2] = pack_bf16(p0, p1);
+                    for (int i = 0; i < HN; i += 2) {
+                        const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
+                        const f2 pp = ((i >> 1) & 3) < POLY_PAIRS ? ex2_poly2(a) : f2{ex2(a.x), ex2(a.y)};
+                        acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
+                        x[i / 2] = pack_bf16(pp.x, pp.y);
+                    }
+                    const f2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+                    ls[0] = s01.x; ls[1] = s01.y; ls[2] = s23.x; ls[3] = s23.y;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < HN; i += 2) {
+                        const float a0 = fmaf(__uint_as_float(x[i]), sc, neg_m);
+                        const float a1 = fmaf(__uint_as_float(x[i + 1]), sc, neg_m);
+                        const float p0 = ((i % EX2_POLY_EVERY) == EX2_POLY_EVERY - 2) ? ex2_poly(a0) : ex2(a0);
+                        const float p1 = (((i + 1) % EX2_POLY_EVERY) == EX2_POLY_EVERY - 1) ? ex2_poly(a1) : ex2(a1);
+                        ls[(i >> 1) & 3] += p0 + p1;
+                        x[i / 2] = pack_bf16(p0, p1);
+                    }
                 }
                 }
                 HI_TR(ttr + 2, j);

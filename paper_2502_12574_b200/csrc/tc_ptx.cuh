@@ -135,6 +135,43 @@ __device__ __forceinline__ float ex2_poly(float x) {
     p = fmaf(p, f, 9.9993026e-1f);
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two fp32 lanes per instruction, half the issue slots).
+struct f2 { float x, y; };
+__device__ __forceinline__ uint64_t f2_bits(f2 a) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ f2 f2_from(uint64_t r) {
+    f2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {  // a * b + c, round-to-nearest
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+    return f2_from(r);
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(r);
+}
+// ex2_poly on a pair with packed arithmetic: 2 FMNMX + 2 FADD2 + 4 FFMA2 + 2 integer adds per 2
+// exponentials (vs 2 MUFU issues that each hold the 4-lane/clk MUFU pipe for 8 cycles per warp).
+__device__ __forceinline__ f2 ex2_poly2(f2 x) {
+    constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23
+    x.x = fmaxf(x.x, -126.f);
+    x.y = fmaxf(x.y, -126.f);
+    const f2 t = fadd2(x, f2{MAGIC, MAGIC});
+    const f2 n = fadd2(t, f2{-MAGIC, -MAGIC});
+    const f2 f = ffma2(n, f2{-1.f, -1.f}, x);
+    f2 q = ffma2(f, f2{5.5160172e-2f, 5.5160172e-2f}, f2{2.4258254e-1f, 2.4258254e-1f});
+    q = ffma2(q, f, f2{6.9326055e-1f, 6.9326055e-1f});
+    q = ffma2(q, f, f2{9.9993026e-1f, 9.9993026e-1f});
+    return f2{__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+              __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23))};
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -240,6 +277,22 @@ __device__ __forceinline__ void umma_bf16_ts_cg2(uint32_t d_tmem, uint32_t a_tme
 }
 // arrive (once each) on the barrier at this shared-memory offset in every CTA of `mask` when all
 // previously issued tcgen05 operations of this thread have completed
+// K/V tile multicast: the box lands at the same shared-memory offset in every CTA of `mask`, and each
+// destination's mbarrier at offset `bar` receives the complete_tx bytes
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z,
+                                               uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "r"(z), "h"(mask)
+        : "memory");
+}
+// single-CTA MMAs' completion signalled to the barrier at offset `bar` in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+                 "h"(mask)
+                 : "memory");
+}
 __device__ __forceinline__ void umma_commit_cg2_mc(uint32_t bar, uint16_t mask) {
     asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
                  "h"(mask)
