@@ -91,6 +91,20 @@ constexpr int EX2_POLY_EVERY = HI_EX2_POLY_EVERY;  // 2 of every 16 exponentials
 #define HI_POLY_PAIRS 0
 #endif
 constexpr int POLY_PAIRS = HI_POLY_PAIRS;
+// Split schedule (SPLIT == 1): P(j) goes to the upper 64 S columns, so QK^T of the next KV tile's first 64
+// keys (S_lo, columns 0-63) can run as soon as the softmax has read S(j) into registers; the softmax
+// releases P in two key halves, so PV(j) over the first 64 keys overlaps the second half's
+// exponentials.  What remains in series per tile is softmax -> PV(j)_hi + S(j+1)_hi (512 cycles of MMA
+// instead of 1024).
+// HI_SPLIT_S = 2: only PV is split (P stays in the lower S columns; S(j+1) is one N = 128 MMA after
+// PV(j)_hi).  Measured: SS MMAs with N = 64 run at 2/3 rate (A + B operand reads exceed SMEM bandwidth,
+// profiles/ubench_mma_rate_r01.txt), so mode 1's S halves cost more than they overlap.
+#ifndef HI_SPLIT_S
+#define HI_SPLIT_S 2
+#endif
+constexpr bool SPLIT_S = HI_SPLIT_S != 0;
+constexpr bool SPLIT_S_LO = HI_SPLIT_S == 1;  // S(j+1)_lo issued early (P in the upper 64 columns)
+constexpr int P_COL = SPLIT_S_LO ? 64 : 0;    // first packed P column
 
 using namespace ptx;
 
@@ -98,6 +112,7 @@ struct __align__(8) Barriers {
     uint64_t q_full;
     uint64_t k_full[NS], v_full[NS], kv_empty[NS];
     uint64_t s_full[2], p_full[2], o_done[2];
+    uint64_t s_cons[2], p_lo[2];  // split schedule: S(j) read into registers / P(j) keys 0-63 stored
     uint32_t tmem_base;
     uint32_t pad;
     float xchg[2][2][BM];   // [tile][half][row]: partial row max, SPLIT=2
@@ -171,6 +186,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto bar_s = [&](int t) { return smem_addr(&bars->s_full[t]); };
     auto bar_p = [&](int t) { return smem_addr(&bars->p_full[t]); };
     auto bar_o = [&](int t) { return smem_addr(&bars->o_done[t]); };
+    auto bar_sc = [&](int t) { return smem_addr(&bars->s_cons[t]); };
+    auto bar_pl = [&](int t) { return smem_addr(&bars->p_lo[t]); };
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
@@ -183,6 +200,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(bar_s(t), 1);
             mbar_init(bar_p(t), 128 * SPLIT);
             mbar_init(bar_o(t), 1);
+            mbar_init(bar_sc(t), 128);
+            mbar_init(bar_pl(t), 128);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -254,6 +273,68 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc_fence_after();
             for (int tt = 0; tt < n_tiles; ++tt)
                 if (nk_t[tt] > 0) issue_s(tt, 0);
+            if constexpr (SPLIT_S) {
+                constexpr uint32_t ID_S64 = idesc_bf16(BM, 64, false);
+                // S_tt(i), keys 64h .. 64h+63 -> S columns [64h, 64h+64): B = rows 64h.. of the K boxes
+                auto issue_s_half = [&](int tt, int i, int h) {
+                    const uint64_t a0 = dq0 + ((tt * (D / 64) * L::BOX) >> 4);
+                    const uint64_t b0 = dk0 + (((i % NS) * (D / 64) * L::BOX + h * 64 * 128) >> 4);
+#pragma unroll
+                    for (int ks = 0; ks < D / 16; ++ks) {
+                        const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
+                        umma_bf16(tmem + tt * 256 + 64 * h, a0 + off, b0 + off, ID_S64, ks > 0);
+                    }
+                };
+                // O_tt += P_tt(j)[keys 64h ..] V(j)[keys 64h ..]; P at packed columns 64 + 32h ..
+                auto issue_pv_half = [&](int tt, int j, int h) {
+                    const uint64_t b0 = dv0 + (((j % NS) * (D / 64) * L::BOX) >> 4);
+#pragma unroll
+                    for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+                        umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + P_COL + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
+                                     (j > 0 || kk > 0 || !first) ? 1u : 0u);
+                };
+                for (int j = 0; j < n_kt; ++j) {
+                    const int s = j % NS;
+                    bool waited_v = false, have_k = false;
+                    for (int tt = 0; tt < n_tiles; ++tt) {
+                        if (j >= nk_t[tt]) continue;
+                        const bool next = j + 1 < nk_t[tt];
+                        bool lo_done = false;
+                        if (next && SPLIT_S_LO) {
+                            // S(j+1)_lo as soon as the softmax holds S(j) in registers -- if K(j+1) has landed
+                            mbar_wait(bar_sc(tt), j & 1);
+                            if (!have_k) have_k = mbar_test(bar_k((j + 1) % NS), ((j + 1) / NS) & 1);
+                            if (have_k) {
+                                tc_fence_after();
+                                issue_s_half(tt, j + 1, 0);
+                                lo_done = true;
+                            }
+                        }
+                        mbar_wait(bar_pl(tt), j & 1);
+                        if (!waited_v) { mbar_wait(bar_v(s), (j / NS) & 1); waited_v = true; }
+                        tc_fence_after();
+                        issue_pv_half(tt, j, 0);
+                        mbar_wait(bar_p(tt), j & 1);
+                        HI_TR_MMA(12 + 2 * tt, j);
+                        tc_fence_after();
+                        issue_pv_half(tt, j, 1);
+                        if (j + 1 == nk_t[tt]) umma_commit(bar_o(tt));
+                        if (next) {
+                            if (!have_k) { mbar_wait(bar_k((j + 1) % NS), ((j + 1) / NS) & 1); have_k = true; }
+                            tc_fence_after();
+                            if (SPLIT_S_LO) {
+                                if (!lo_done) issue_s_half(tt, j + 1, 0);
+                                issue_s_half(tt, j + 1, 1);
+                                umma_commit(bar_s(tt));
+                            } else {
+                                issue_s(tt, j + 1);  // commits s_full
+                            }
+                            HI_TR_MMA(12 + 2 * tt + 1, j);
+                        }
+                    }
+                    umma_commit(bar_e(s));  // K(j), V(j) consumed by every tile
+                }
+            } else {
             for (int j = 0; j < n_kt; ++j) {
                 const int s = j % NS;
                 bool waited_v = false, waited_k = false;
@@ -272,6 +353,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
                 umma_commit(bar_e(s));  // K(j), V(j) consumed by every tile
+            }
             }
         }
     } else {
@@ -338,6 +420,60 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < HN; ++i)
                         if (key0 + i > lim2) x[i] = __float_as_uint(-CUDART_INF_F);
+                }
+                if constexpr (SPLIT_S) {
+                    if constexpr (SPLIT_S_LO) {  // S(j) is in registers: columns 0-63 may take S(j+1)_lo
+                        tc_fence_before();
+                        mbar_arrive(bar_sc(tt));
+                    }
+                    float mk[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) mk[c] = __uint_as_float(x[c]);
+#pragma unroll
+                    for (int i = 8; i < HN; i += 8)
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) mk[c] = fmaxf(mk[c], __uint_as_float(x[i + c]));
+                    const float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])), fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
+                    const float mxs = mx * sc;
+                    const bool grw = (mx != -CUDART_INF_F) && (m_run == -CUDART_INF_F || mxs > m_run + RESCALE_THRESHOLD);
+                    const float mref = grw ? mxs : m_run;
+                    const float alp = grw ? ((m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mxs)) : 1.f;
+                    HI_TR(ttr + 1, j);
+                    // O correction before PV(j)_lo may accumulate (PV(j-1) is complete: S(j) was issued after it)
+                    if ((!first || j > 0) && __any_sync(0xffffffffu, grw)) {
+#pragma unroll
+                        for (int cb = 0; cb < HD / 32; ++cb) {
+                            uint32_t v[32];
+                            tmem_ld32(t_o + cb * 32, v);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alp);
+                            tmem_st32(t_o + cb * 32, v);
+                        }
+                    }
+                    const float nm = (mref == -CUDART_INF_F) ? 0.f : -mref;
+                    const f2 sc2{sc, sc}, nm2{nm, nm};
+                    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                        for (int i = 64 * h; i < 64 * h + 64; i += 2) {
+                            const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
+                            const f2 pp{ex2(a.x), ex2(a.y)};
+                            acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
+                            x[i / 2] = pack_bf16(pp.x, pp.y);
+                        }
+                        // P keys [64h, 64h+64) -> packed columns [P_COL + 32h, P_COL + 32h + 32)
+                        tmem_st32(t_s + P_COL + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(&x[32 * h]));
+                        tmem_wait_st();
+                        tc_fence_before();
+                        mbar_arrive(h == 0 ? bar_pl(tt) : bar_p(tt));
+                        HI_TR(ttr + 2 + 2 * h, j);
+                    }
+                    const f2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+                    l_run = l_run * alp + ((s01.x + s01.y) + (s23.x + s23.y));
+                    m_run = mref;
+                    continue;
                 }
                 float m_ref = m_run, alpha = 1.f;
                 bool grow = false;

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256, 1) kern(int iters, long long* cyc, int bg
                     for (int kk = 0; kk < 8; ++kk)
                         umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, dv + ((kk * 16 * 128) >> 4), ID_O, 1u);
                 }
-                if (MODE >= 5) {  // S + PV with (MODE - 4) commits per iteration to never-waited barriers
+                if (MODE >= 5 && MODE <= 8) {  // S + PV with (MODE - 4) commits per iteration to never-waited barriers
 #pragma unroll
                     for (int ks = 0; ks < 8; ++ks) {
                         const uint32_t off = ((ks >> 2) * BOX + (ks & 3) * 32) >> 4;
@@ -63,6 +63,39 @@ __global__ void __launch_bounds__(256, 1) kern(int iters, long long* cyc, int bg
                     for (int kk = 0; kk < 8; ++kk)
                         umma_bf16_ts(tmem + 128, tmem + kk * 8, dv + ((kk * 16 * 128) >> 4), ID_O, 1u);
                     for (int c = 1; c < MODE - 4; ++c) umma_commit(smem_addr(&cbar[c]));
+                }
+                if (MODE == 9) {  // SS M128 N64 K128 (8 x K16)
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint32_t off = ((ks >> 2) * BOX + (ks & 3) * 32) >> 4;
+                        umma_bf16(tmem, dq + off, dk + off, idesc_bf16(128, 64, false), ks > 0);
+                    }
+                }
+                if (MODE == 10) {  // TS M128 N128 K64 (4 x K16)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_bf16_ts(tmem + 128, tmem + kk * 8, dv + ((kk * 16 * 128) >> 4), ID_O, 1u);
+                }
+                if (MODE == 11 || MODE == 13) {  // SS N128 / N256, K64 (4 x K16)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const uint32_t off = ((ks >> 2) * BOX + (ks & 3) * 32) >> 4;
+                        umma_bf16(tmem, dq + off, dk + off, MODE == 11 ? ID_S : ID_S256, ks > 0);
+                    }
+                }
+                if (MODE == 12) {  // SS N64, 16 x K16
+#pragma unroll
+                    for (int ks = 0; ks < 16; ++ks) {
+                        const uint32_t off = (((ks & 7) >> 2) * BOX + (ks & 3) * 32) >> 4;
+                        umma_bf16(tmem, dq + off, dk + off, idesc_bf16(128, 64, false), ks > 0);
+                    }
+                }
+                if (MODE == 14) {  // SS N64 K128 into two alternating D (cols 0 / 64)
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint32_t off = ((ks >> 2) * BOX + (ks & 3) * 32) >> 4;
+                        umma_bf16(tmem + (it & 1) * 64, dq + off, dk + off, idesc_bf16(128, 64, false), ks > 0);
+                    }
                 }
                 if (MODE == 3) {
 #pragma unroll
@@ -156,6 +189,12 @@ int main() {
     run<1>("PV: TS M128 N128 K128 (A in TMEM)", 1, 2);
     run<2>("S + PV (one tile)", 2, 2);
     run<2>("S + PV (one tile)", 2, 3);
+    run<9>("SS M128 N64 K128", 0.5);
+    run<11>("SS M128 N128 K64", 0.5);
+    run<13>("SS M128 N256 K64", 1);
+    run<12>("SS M128 N64 K256", 1);
+    run<14>("SS M128 N64 K128 alternating D", 0.5);
+    run<10>("TS M128 N128 K64", 0.5);
     run<5>("S + PV, 1 commit / iter", 2);
     run<6>("S + PV, 2 commits / iter", 2);
     run<8>("S + PV, 4 commits / iter", 2);
