@@ -32,6 +32,7 @@
 
 #include <cstdio>
 #include <mutex>
+#include <type_traits>
 
 namespace hi {
 namespace {
@@ -105,6 +106,12 @@ constexpr int POLY_PAIRS = HI_POLY_PAIRS;
 constexpr bool SPLIT_S = HI_SPLIT_S != 0;
 constexpr bool SPLIT_S_LO = HI_SPLIT_S == 1;  // S(j+1)_lo issued early (P in the upper 64 columns)
 constexpr int P_COL = SPLIT_S_LO ? 64 : 0;    // first packed P column
+// keys whose P is released first (PV(j)_lo covers them; only PV over the rest stays on the chain)
+#ifndef HI_P_SPLIT_KEYS
+#define HI_P_SPLIT_KEYS 64
+#endif
+constexpr int KS = HI_P_SPLIT_KEYS;
+static_assert(KS == 64 || KS == 96, "P split at 64 or 96 keys");
 
 using namespace ptx;
 
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 auto issue_pv_half = [&](int tt, int j, int h) {
                     const uint64_t b0 = dv0 + (((j % NS) * (D / 64) * L::BOX) >> 4);
 #pragma unroll
-                    for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+                    for (int kk = (h ? KS / 16 : 0); kk < (h ? BN / 16 : KS / 16); ++kk)
                         umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + P_COL + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                      (j > 0 || kk > 0 || !first) ? 1u : 0u);
                 };
@@ -454,22 +461,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const float nm = (mref == -CUDART_INF_F) ? 0.f : -mref;
                     const f2 sc2{sc, sc}, nm2{nm, nm};
                     f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+                    // exponentials of keys [LO, HI) packed in place (x[i/2]); compile-time bounds keep x[] in
+                    // registers
+                    auto exp_keys = [&](auto lo_c, auto hi_c) {
+                        constexpr int LO = decltype(lo_c)::value, HI = decltype(hi_c)::value;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                        for (int i = 64 * h; i < 64 * h + 64; i += 2) {
+                        for (int i = LO; i < HI; i += 2) {
                             const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
                             const f2 pp{ex2(a.x), ex2(a.y)};
                             acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
                             x[i / 2] = pack_bf16(pp.x, pp.y);
                         }
-                        // P keys [64h, 64h+64) -> packed columns [P_COL + 32h, P_COL + 32h + 32)
-                        tmem_st32(t_s + P_COL + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(&x[32 * h]));
+                    };
+                    auto release_p = [&](uint32_t bar) {
                         tmem_wait_st();
                         tc_fence_before();
-                        mbar_arrive(h == 0 ? bar_pl(tt) : bar_p(tt));
-                        HI_TR(ttr + 2 + 2 * h, j);
-                    }
+                        mbar_arrive(bar);
+                    };
+                    // keys [0, KS) -> packed columns [P_COL, P_COL + KS/2): PV(j)_lo may start
+                    exp_keys(std::integral_constant<int, 0>{}, std::integral_constant<int, KS>{});
+                    tmem_st32(t_s + P_COL, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                    if constexpr (KS == 96) tmem_st16(t_s + P_COL + 32, &x[32]);
+                    release_p(bar_pl(tt));
+                    HI_TR(ttr + 2, j);
+                    // keys [KS, 128) -> packed columns [P_COL + KS/2, P_COL + 64)
+                    exp_keys(std::integral_constant<int, KS>{}, std::integral_constant<int, BN>{});
+                    if constexpr (KS == 64) tmem_st32(t_s + P_COL + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));
+                    else tmem_st16(t_s + P_COL + 48, &x[48]);
+                    release_p(bar_p(tt));
+                    HI_TR(ttr + 4, j);
                     const f2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
                     l_run = l_run * alp + ((s01.x + s01.y) + (s23.x + s23.y));
                     m_run = mref;
