@@ -113,6 +113,71 @@ int oracle_attention_rows(const uint16_t* q_rows, int64_t n_rows, int64_t q_stri
     return err;
 }
 
+/*
+ * oracle_attention_rows_duo -- the same row attention for a duo-attention STREAMING head
+ * (NEXT-3; §4 "truncating less important heads to a fixed length", App. D;
+ * DuoAttention's streaming heads keep the attention-sink tokens and a window of recent tokens,
+ * reading R18 in DESIGN.md).  A query row at position p attends exactly the keys
+ *       V(p) = { i : i <= p  and  ( i < n_sink  or  i > p - win ) }
+ * (win <= 0: no truncation, V(p) = {0..p}, the retrieval-head rule above), written out as
+ *       s_i = (q . k_i) / sqrt(d)   i in V(p)
+ *       m = max_{i in V(p)} s_i;  w_i = exp(s_i - m);  o = sum w_i v_i / sum w_i
+ * in key order, fp64, no blocking.  Arguments as oracle_attention_rows.
+ */
+int oracle_attention_rows_duo(const uint16_t* q_rows, int64_t n_rows, int64_t q_stride,
+                              const int64_t* last_key, int64_t n_sink, int64_t win,
+                              const uint16_t* K, const uint16_t* V, int64_t n_keys, int64_t kv_stride,
+                              int d, double* out) {
+    if (n_rows < 0 || d <= 0 || n_keys < 0 || n_sink < 0) return -1;
+    for (int64_t r = 0; r < n_rows; ++r)
+        if (last_key[r] < 0 || last_key[r] >= n_keys) return -1;
+    int err = 0;
+    const double inv_sqrt_d = 1.0 / sqrt((double)d);
+#pragma omp parallel
+    {
+        double* q = (double*)malloc(sizeof(double) * (size_t)d);
+        double* acc = (double*)malloc(sizeof(double) * (size_t)d);
+        if (!q || !acc) {
+#pragma omp atomic write
+            err = -2;
+        }
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t r = 0; r < n_rows; ++r) {
+            if (err) continue;
+            const int64_t p = last_key[r];
+            for (int c = 0; c < d; ++c) q[c] = bf16_bits_to_double(q_rows[r * q_stride + c]);
+            /* m = max over the visible keys of s_i (first pass), then the weighted sum (second pass) */
+            double m = 0.0;
+            int have = 0;
+            for (int64_t i = 0; i <= p; ++i) {
+                if (!(win <= 0 || i < n_sink || i > p - win)) continue;
+                const uint16_t* k = K + i * kv_stride;
+                double dot = 0.0;
+                for (int c = 0; c < d; ++c) dot += q[c] * bf16_bits_to_double(k[c]);
+                const double si = dot * inv_sqrt_d;
+                if (!have || si > m) m = si;
+                have = 1;
+            }
+            double wsum = 0.0;
+            for (int c = 0; c < d; ++c) acc[c] = 0.0;
+            for (int64_t i = 0; i <= p; ++i) {
+                if (!(win <= 0 || i < n_sink || i > p - win)) continue;
+                const uint16_t* k = K + i * kv_stride;
+                double dot = 0.0;
+                for (int c = 0; c < d; ++c) dot += q[c] * bf16_bits_to_double(k[c]);
+                const double w = exp(dot * inv_sqrt_d - m);
+                const uint16_t* v = V + i * kv_stride;
+                wsum += w;
+                for (int c = 0; c < d; ++c) acc[c] += w * bf16_bits_to_double(v[c]);
+            }
+            for (int c = 0; c < d; ++c) out[r * d + c] = acc[c] / wsum;
+        }
+        free(q);
+        free(acc);
+    }
+    return err;
+}
+
 /* Threads the OpenMP runtime will use (reported as cpu_baseline.cores). */
 int oracle_num_threads(void) {
 #ifdef _OPENMP

@@ -53,6 +53,11 @@ def _load():
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
             ctypes.c_int, ctypes.c_void_p]
+        lib.oracle_attention_rows_duo.restype = ctypes.c_int
+        lib.oracle_attention_rows_duo.argtypes = [
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+            ctypes.c_int, ctypes.c_void_p]
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -86,6 +91,42 @@ def attention_rows(q_rows: np.ndarray, last_key: np.ndarray, k: np.ndarray, v: n
     return out
 
 
+def attention_rows_duo(q_rows: np.ndarray, last_key: np.ndarray, k: np.ndarray, v: np.ndarray,
+                       n_sink: int, win: int) -> np.ndarray:
+    """attention_rows for a duo-attention streaming head: row p attends keys i <= p with i < n_sink or
+    i > p - win (oracle_attention_rows_duo; win <= 0 = no truncation)."""
+    lib = _load()
+    q_rows = np.ascontiguousarray(q_rows, dtype=np.uint16)
+    last_key = np.ascontiguousarray(last_key, dtype=np.int64)
+    k = np.ascontiguousarray(k, dtype=np.uint16)
+    v = np.ascontiguousarray(v, dtype=np.uint16)
+    n_rows, d = q_rows.shape
+    out = np.empty((n_rows, d), dtype=np.float64)
+    rc = lib.oracle_attention_rows_duo(q_rows.ctypes.data, n_rows, d, last_key.ctypes.data, int(n_sink), int(win),
+                                       k.ctypes.data, v.ctypes.data, k.shape[0], d, d, out.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(f"oracle_attention_rows_duo failed: {rc}")
+    return out
+
+
+def duo_gqa_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, q_pos0: int, streaming,
+                      n_sink: int, win: int) -> np.ndarray:
+    """gqa_attention with duo-attention head-wise sparsity (NEXT-3): kv heads h with streaming[h]
+    true attend the sink + recent-window key set; the others (retrieval heads) full causal."""
+    n_q, hq, d = q.shape
+    n_k, hkv, _ = k.shape
+    g = hq // hkv
+    out = np.empty((n_q, hq, d), dtype=np.float64)
+    last = np.arange(q_pos0, q_pos0 + n_q, dtype=np.int64)
+    for j in range(hq):
+        h = j // g
+        if streaming[h]:
+            out[:, j, :] = attention_rows_duo(q[:, j, :], last, k[:, h, :], v[:, h, :], n_sink, win)
+        else:
+            out[:, j, :] = attention_rows(q[:, j, :], last, k[:, h, :], v[:, h, :])
+    return out
+
+
 def gqa_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, q_pos0: int) -> np.ndarray:
     """Head-wise causal GQA attention (Eq. 9 + concat).
 
@@ -107,9 +148,11 @@ def gqa_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, q_pos0: int) -> n
     return out
 
 
-def dense_attention_np(q: np.ndarray, k: np.ndarray, v: np.ndarray, q_pos0: int) -> np.ndarray:
+def dense_attention_np(q: np.ndarray, k: np.ndarray, v: np.ndarray, q_pos0: int, streaming=None,
+                       n_sink: int = 0, win: int = 0) -> np.ndarray:
     """Textbook brute force (Eq. 3): full score matrix, bottom-right causal mask, row softmax.
-    Same shapes/semantics as gqa_attention; float64 numpy throughout."""
+    Same shapes/semantics as gqa_attention; float64 numpy throughout.  With ``streaming`` (per kv
+    head) the streaming heads' mask is additionally restricted to keys < n_sink or > p - win."""
     from synth import bf16_to_f64
     qf, kf, vf = bf16_to_f64(q), bf16_to_f64(k), bf16_to_f64(v)
     n_q, hq, d = qf.shape
@@ -120,7 +163,13 @@ def dense_attention_np(q: np.ndarray, k: np.ndarray, v: np.ndarray, q_pos0: int)
     scores = np.einsum("qhd,khd->hqk", qf, kf) / np.sqrt(d)
     qpos = np.arange(q_pos0, q_pos0 + n_q)[:, None]
     kpos = np.arange(n_k)[None, :]
-    scores = np.where((kpos <= qpos)[None], scores, -np.inf)
+    mask = np.broadcast_to((kpos <= qpos)[None], scores.shape).copy()
+    if streaming is not None and win > 0:
+        duo = (kpos < n_sink) | (kpos > qpos - win)
+        for j in range(hq):
+            if streaming[j // g]:
+                mask[j] &= duo
+    scores = np.where(mask, scores, -np.inf)
     scores = scores - scores.max(axis=-1, keepdims=True)
     w = np.exp(scores)
     w = w / w.sum(axis=-1, keepdims=True)

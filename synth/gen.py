@@ -111,3 +111,17 @@ def gen_qkv(seed: int, dist: str, layer: int, pos0: int, n_pos: int,
     k = gen_block(seed, TENSOR_K, dist, layer, kv_head0, kv_heads, pos0, n_pos, d)
     v = gen_block(seed, TENSOR_V, dist, layer, kv_head0, kv_heads, pos0, n_pos, d)
     return q, k, v
+
+
+def streaming_labels(seed: int, layers: int, kv_heads: int, frac: float = 0.5) -> np.ndarray:
+    """Synthetic duo-attention head labels (NEXT-3; the paper's labels come from a trained model,
+    App. D): uint8 [layers, kv_heads], 1 = streaming head.  Exactly round(frac * kv_heads)
+    streaming heads per layer, chosen by ranking a counter hash of (seed, layer, head) -- a pure
+    function of its arguments, no method arithmetic."""
+    n_str = int(round(frac * kv_heads))
+    lab = np.zeros((layers, kv_heads), dtype=np.uint8)
+    for layer in range(layers):
+        keys = np.array([(seed << 20) ^ (layer << 8) ^ h for h in range(kv_heads)], dtype=np.uint64)
+        order = np.argsort(splitmix64(keys), kind="stable")
+        lab[layer, order[:n_str]] = 1
+    return lab

@@ -52,3 +52,13 @@ def test_bf16_rne_ties():
     # 1 + 2^-8 is a tie between 1.0 and 1+2^-7: RNE keeps the even mantissa (1.0)
     f = np.array([1.0 + 2.0 ** -8, 1.0 + 3 * 2.0 ** -8, -1.5], dtype=np.float32)
     assert list(synth.f32_to_bf16_rne(f)) == [0x3F80, 0x3F82, 0xBFC0]
+
+
+def test_streaming_labels_deterministic_and_balanced():
+    a = synth.streaming_labels(7, 32, 8, 0.5)
+    b = synth.streaming_labels(7, 32, 8, 0.5)
+    assert a.dtype == np.uint8 and a.shape == (32, 8)
+    assert np.array_equal(a, b)
+    assert np.all(a.sum(axis=1) == 4)
+    assert not np.array_equal(a, synth.streaming_labels(8, 32, 8, 0.5))
+    assert synth.streaming_labels(1, 2, 8, 0.0).sum() == 0 and synth.streaming_labels(1, 2, 8, 1.0).sum() == 16
