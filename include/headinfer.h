@@ -74,6 +74,17 @@ typedef struct hi_options {
                               head_group heads at max_ctx.  Must divide kv_heads/world, or be
                               HI_GROUP_AUTO (-1): the smallest divisor whose chunk launch fills
                               >= 8 waves of 128-row tiles, staging capped at 1/32 of HBM. */
+    /* NEXT-3 head-wise sparsity (duo-attention, §4; App. D; Tab. "Prefill 1M, Decoding
+     * with 1M KV cache" P:L988-1000): streaming_heads points at layers*kv_heads bytes (GLOBAL kv head index,
+     * layer-major; the context reads its shard), nonzero = streaming head.  A streaming head is never
+     * offloaded: its K/V live in HBM as duo_sink attention-sink rows plus a ring of the duo_window most
+     * recent rows ("keep the streaming head in the GPU"), and a query at position p attends exactly
+     * the keys i <= p with i < duo_sink or i > p - duo_window (reading R18).  The other (retrieval) heads
+     * keep the full cache and are offloaded / resident / grouped as above.  The caller's array is copied.
+     * NULL (default) = no streaming heads. */
+    const unsigned char* streaming_heads;
+    int duo_sink;         /* attention-sink tokens kept by streaming heads: 0 = default 64, < 0 = none */
+    int duo_window;       /* recent-window tokens kept by streaming heads (>= 1): 0 = default 256 */
 } hi_options;
 
 #define HI_RESIDENT_AUTO (-1)
@@ -114,6 +125,8 @@ typedef struct hi_stats {
     int resident_kv_heads;        /* H_on pairs held in HBM (NEXT-1) */
     int64_t resident_bytes;       /* their device KV bytes */
     int head_group;               /* kv heads per offload unit (NEXT-2) */
+    int streaming_kv_heads;       /* local (layer, kv head) pairs that are duo streaming heads (NEXT-3) */
+    int64_t streaming_bytes;      /* their device sink + window KV bytes */
 } hi_stats;
 
 /*
@@ -168,13 +181,15 @@ hi_status hi_free(hi_ctx* ctx);
 
 /* Copy KV rows [pos, pos+n) of (layer, local kv head) into host buffers k_dst, v_dst ([n, head_dim]
  * bf16 each) from wherever they live (host store, or HBM for resident pairs).  Waits for pending
- * write-backs first.  HI_ESHAPE on bad range. */
+ * write-backs first.  HI_ESHAPE on bad range.  Streaming heads (NEXT-3) hold only rows p < duo_sink and
+ * the last duo_window rows below seq_len; asking for any other row is HI_ESTATE. */
 hi_status hi_read_host_kv(hi_ctx* ctx, int layer, int kv_head_local, int64_t pos, int64_t n,
                           void* k_dst, void* v_dst);
 
 /* Write host KV rows [pos, pos+n) of (layer, local kv head) from k_src, v_src ([n, head_dim]
  * bf16 each; device pointers if from_device != 0, else host).  Synchronous.  Does not move
- * seq_len.  This is the "helper for simulating or preparing decoding with large context"
+ * seq_len.  For a streaming head (NEXT-3) rows p < duo_sink go to its sink and rows p >= duo_sink to its
+ * window ring (only the last duo_window of the range are kept).  This is the "helper for simulating or preparing decoding with large context"
  * (App. E): benches fill a long history without timing a full prefill. */
 hi_status hi_write_host_kv(hi_ctx* ctx, int layer, int kv_head_local, int64_t pos, int64_t n,
                            const void* k_src, const void* v_src, int from_device);

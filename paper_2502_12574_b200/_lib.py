@@ -35,7 +35,8 @@ EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", 
 class hi_options(ctypes.Structure):
     _fields_ = [("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64), ("device", ctypes.c_int),
                 ("flags", ctypes.c_int), ("numa_policy", ctypes.c_int), ("numa_node", ctypes.c_int),
-                ("resident_kv_heads", ctypes.c_int), ("head_group", ctypes.c_int)]
+                ("resident_kv_heads", ctypes.c_int), ("head_group", ctypes.c_int),
+                ("streaming_heads", ctypes.c_void_p), ("duo_sink", ctypes.c_int), ("duo_window", ctypes.c_int)]
 
 
 class hi_stats(ctypes.Structure):
@@ -50,7 +51,8 @@ class hi_stats(ctypes.Structure):
                 ("init_seconds", ctypes.c_double),
                 ("numa_node", ctypes.c_int), ("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64),
                 ("resident_kv_heads", ctypes.c_int), ("resident_bytes", ctypes.c_int64),
-                ("head_group", ctypes.c_int)]
+                ("head_group", ctypes.c_int),
+                ("streaming_kv_heads", ctypes.c_int), ("streaming_bytes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

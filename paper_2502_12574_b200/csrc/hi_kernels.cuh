@@ -21,6 +21,7 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const cuuint64_t
 // log2 domain: x = (q.k) * log2(e)/sqrt(d); m is the running max of x, l = sum 2^(x-m),
 // O = sum 2^(x-m) v.  FIRST initialises the state, LAST writes out = O / l as bf16.
 enum PrefillFlags : int { PF_FIRST = 1, PF_LAST = 2, PF_CAUSAL = 4 };
+constexpr int MAX_LAUNCH_HEADS = 64;  // kv heads one launch may cover (and the cap on kv_heads/world)
 
 struct PrefillParams {
     const __nv_bfloat16* q;   // (token 0, first q head of the group); row (t,j) at q + t*q_tok_stride + j*d
@@ -45,7 +46,21 @@ struct PrefillParams {
     int n_heads;              // 1 = one kv head (k_prefill_mma.cu / k_prefill_tc2.cu support only 1)
     int64_t kv_head_stride;   // elements
     int64_t state_rows;       // rows of O/m/l state per head (>= n_q*g)
+    // head maps (any set of kv heads per launch): blockIdx.y = hh takes q/out columns of kv head head_q[hh]
+    // (q heads head_q[hh]*g ..), keys at k/v + head_kv[hh]*kv_head_stride, state rows hh*state_rows; the q/out
+    // tensor map spans q_span kv heads' q columns, the k/v map kv_span heads.  set_identity_heads() = h0 + hh.
+    int16_t head_q[MAX_LAUNCH_HEADS];
+    int16_t head_kv[MAX_LAUNCH_HEADS];
+    int q_span, kv_span;
+    // NEXT-3 duo-attention streaming heads (reading R18): win > 0 restricts key i of the segment to
+    // i > p - win for query position p (the recent window).  The runtime only passes win > 0 for segments
+    // that hold no sink keys (k_pos0 >= n_sink); sink segments are plain (all visible).
+    int win;
 };
+inline void set_identity_heads(PrefillParams& p, int n) {
+    for (int i = 0; i < n && i < MAX_LAUNCH_HEADS; ++i) p.head_q[i] = p.head_kv[i] = static_cast<int16_t>(i);
+    p.q_span = p.kv_span = n;
+}
 // sm_100a kernels: TMA + tcgen05.mma + TMEM.  k_prefill_tc.cu: one CTA per 256 rows (any head_dim) --
 // the product path; k_prefill_tc2.cu: CTA pairs (cta_group::2, M = 256), head_dim 128, HI_FLAG_PREFILL_2CTA
 cudaError_t launch_prefill_tc2(const PrefillParams& p, int d, cudaStream_t stream);
@@ -68,7 +83,17 @@ struct DecodePartialParams {
     int64_t kv_head_stride;   // elements between head h and h+1 in k and in v (0 when n_heads == 1)
     int64_t q_head_stride;    // elements between the q groups of consecutive heads (g*d)
     int64_t parts_head_stride;// floats between the record arrays of consecutive heads
+    // head maps: blockIdx.y = y reads q group head[y] (q + head[y]*q_head_stride), writes records at
+    // parts + head[y]*parts_head_stride, and streams keys of k/v head coordinate kvc[y] (stride
+    // kv_head_stride; the tensor map spans kv_span heads)
+    int16_t head[MAX_LAUNCH_HEADS];
+    int16_t kvc[MAX_LAUNCH_HEADS];
+    int kv_span;
 };
+inline void set_identity_heads(DecodePartialParams& p, int n) {
+    for (int i = 0; i < n && i < MAX_LAUNCH_HEADS; ++i) p.head[i] = p.kvc[i] = static_cast<int16_t>(i);
+    p.kv_span = n;
+}
 cudaError_t launch_decode_partial(const DecodePartialParams& p, int d, int g, int n_splits, int n_heads,
                                   cudaStream_t stream);
 
@@ -78,9 +103,7 @@ struct DecodeCombineParams {
     const __nv_bfloat16* v_new;  // [Hkv_loc][d]
     const float* parts;          // [Hkv_loc][max_parts][g][d+4]
     int max_parts;
-    int n_parts;                 // parts per kv head for local kv heads h >= h_lo (offloaded)
-    int n_parts_lo;              // parts per kv head for h < h_lo (HBM-resident heads, NEXT-1)
-    int h_lo;
+    int16_t n_parts[MAX_LAUNCH_HEADS];  // records per local kv head (offloaded / resident / streaming differ)
     int g;
     float scale_log2;
     __nv_bfloat16* out;          // [Hq_loc][d]
@@ -90,6 +113,23 @@ cudaError_t launch_decode_combine(const DecodeCombineParams& p, int d, int hq_lo
 // ---- pack the chunk's K and V [n][Hkv][d] into head-major [Hkv][2][n][d] (a2, K5b) ------
 cudaError_t launch_pack_kv(const __nv_bfloat16* k, const __nv_bfloat16* v, __nv_bfloat16* packed,
                            int n, int hkv, int d, cudaStream_t stream);
+
+// ---- NEXT-3: append new K/V rows of the duo streaming heads into their device sink + ring buffers ----
+// For each listed kv head heads[y] and new position p in [pos0, pos0+n): rows p < n_sink go to sink row p,
+// rows p >= max(n_sink, pos0+n-ring) to ring row n_sink + (p-n_sink) % ring (the rest are overwritten in the
+// same call and skipped).  Source row (y, t) at src_k/src_v + heads[y]*src_head_stride + t*src_row_stride;
+// destination head h at dst + h*dst_head_stride (K rows, then V rows dst_v_off elements later).
+struct DuoAppendParams {
+    const __nv_bfloat16* src_k;
+    const __nv_bfloat16* src_v;
+    int64_t src_head_stride, src_row_stride;
+    __nv_bfloat16* dst;
+    int64_t dst_head_stride, dst_v_off;
+    int64_t pos0;
+    int n, n_sink, ring, n_heads;
+    int16_t heads[MAX_LAUNCH_HEADS];
+};
+cudaError_t launch_duo_append(const DuoAppendParams& p, int d, cudaStream_t stream);
 
 // ---- fill with a NaN bit pattern (poison mode, race detection) --------------------------
 cudaError_t launch_poison(void* ptr, size_t bytes, cudaStream_t stream);

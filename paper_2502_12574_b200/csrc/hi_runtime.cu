@@ -63,8 +63,11 @@ struct hi_ctx {
     std::vector<int64_t> seq_len;
     bool sticky = false;
     std::string err = "no error";
-    // (a) host KV store (offloaded pairs) + device-resident KV cache (H_on pairs, NEXT-1)
-    int n_res = 0;                     // (layer, kv head) pairs in layer-major order < n_res stay in HBM
+    // (a) host KV store (offloaded pairs) + device-resident KV cache (H_on pairs, NEXT-1).  Pairs are numbered
+    // over the RETRIEVAL (layer, kv head) pairs only, layer-major (cidx); duo streaming pairs (NEXT-3) get -1.
+    std::vector<int> cidx;             // [L*Hkv_loc]
+    int n_retr = 0;                    // retrieval pairs
+    int n_res = 0;                     // retrieval pairs with cidx < n_res stay in HBM
     uint8_t* d_res = nullptr;
     size_t res_bytes = 0;
     uint8_t* host = nullptr;
@@ -94,6 +97,15 @@ struct hi_ctx {
     int max_parts = 0;
     __nv_bfloat16* d_kvnew = nullptr;  // [L][2][Hkv_loc][d]
     size_t workspace_bytes = 0;
+    // NEXT-3 duo streaming heads: per (layer, kv head) a device block [K: duo_rows x d | V: duo_rows x d],
+    // rows [0, duo_sink) = sink positions, rows duo_sink + (p - duo_sink) % duo_ring = the recent window
+    int duo_sink = 0, duo_win = 0, duo_ring = 0, n_stream = 0;
+    int64_t duo_rows = 0;
+    uint8_t* d_duo = nullptr;
+    size_t duo_bytes = 0;
+    // per-layer head lists (local kv heads, ascending): resident retrieval, offload units, streaming
+    std::vector<std::vector<int>> res_heads, str_heads;
+    std::vector<std::vector<std::vector<int>>> off_units;
     // (f) stats
     int64_t h2d_bytes = 0, d2h_bytes = 0, prefill_calls = 0, decode_calls = 0, launches = 0;
     double init_seconds = 0.0;
@@ -103,11 +115,9 @@ struct hi_ctx {
     double prefill_ms = 0, prefill_flops = 0, decode_ms = 0, decode_bytes = 0;
     int64_t prefill_timed = 0, decode_timed = 0;
 
-    size_t pair(int layer, int h) const { return static_cast<size_t>(layer) * Hkv_loc + h; }
-    bool resident(int layer, int h) const { return pair(layer, h) < static_cast<size_t>(n_res); }
-    int resident_heads_of_layer(int layer) const {  // resident pairs of a layer are its first heads
-        return std::max(0, std::min(Hkv_loc, n_res - layer * Hkv_loc));
-    }
+    size_t pair(int layer, int h) const { return static_cast<size_t>(cidx[static_cast<size_t>(layer) * Hkv_loc + h]); }
+    bool streaming(int layer, int h) const { return cidx[static_cast<size_t>(layer) * Hkv_loc + h] < 0; }
+    bool resident(int layer, int h) const { return !streaming(layer, h) && pair(layer, h) < static_cast<size_t>(n_res); }
     uint8_t* host_k(int layer, int h, int64_t row) const {
         return host + ((pair(layer, h) - n_res) * 2 + 0) * static_cast<size_t>(max_ctx) * d * 2 +
                static_cast<size_t>(row) * d * 2;
@@ -122,6 +132,13 @@ struct hi_ctx {
     uint8_t* dev_v(int layer, int h, int64_t row) const {
         return d_res + (pair(layer, h) * 2 + 1) * static_cast<size_t>(max_ctx) * d * 2 + static_cast<size_t>(row) * d * 2;
     }
+    // streaming head block: [K rows | V rows], duo_rows each
+    size_t duo_head_elems() const { return static_cast<size_t>(2) * duo_rows * d; }
+    __nv_bfloat16* duo_k(int layer, int h, int64_t row) const {
+        return reinterpret_cast<__nv_bfloat16*>(d_duo) + (static_cast<size_t>(layer) * Hkv_loc + h) * duo_head_elems() +
+               static_cast<size_t>(row) * d;
+    }
+    int64_t duo_row(int64_t pos) const { return pos < duo_sink ? pos : duo_sink + (pos - duo_sink) % duo_ring; }
     // where the KV rows of (layer, h) live: device cache (resident) or host store (offloaded)
     uint8_t* kv_k(int layer, int h, int64_t row) const { return resident(layer, h) ? dev_k(layer, h, row) : host_k(layer, h, row); }
     uint8_t* kv_v(int layer, int h, int64_t row) const { return resident(layer, h) ? dev_v(layer, h, row) : host_v(layer, h, row); }
@@ -245,6 +262,7 @@ void destroy(hi_ctx* c) {
     cudaFree(c->d_parts);
     cudaFree(c->d_kvnew);
     cudaFree(c->d_res);
+    cudaFree(c->d_duo);
     if (c->host) {
         if (c->host_registered) cudaHostUnregister(c->host);
         munmap(c->host, c->host_map_bytes);
@@ -267,24 +285,40 @@ int64_t decode_parts_for_block(int64_t nk) {
     return (nk + sl - 1) / sl;
 }
 
+// Visible (query, key) pairs of one prefill segment (the launch's algorithmic work, HI_FLAG_TIMING): token t
+// (position q_pos0 + t) sees key position k in [k_pos0, k_pos0 + n_k) iff (not causal or k <= p) and
+// (win <= 0 or k > p - win).
+double seg_pairs(int64_t q_pos0, int n, int64_t k_pos0, int64_t n_k, bool causal, int win) {
+    if (!causal && win <= 0) return static_cast<double>(n) * static_cast<double>(n_k);
+    double tot = 0.0;
+    for (int t = 0; t < n; ++t) {
+        const int64_t p = q_pos0 + t;
+        const int64_t hi = causal ? std::min(k_pos0 + n_k - 1, p) : k_pos0 + n_k - 1;
+        const int64_t lo = win > 0 ? std::max(k_pos0, p - win + 1) : k_pos0;
+        if (hi >= lo) tot += static_cast<double>(hi - lo + 1);
+    }
+    return tot;
+}
+
 cudaError_t launch_prefill(hi_ctx* c, const hi::PrefillParams& p) {
     const bool mma = c->flags & HI_FLAG_MMA_SYNC_PREFILL;
     const bool pair = !mma && c->d == 128 && (c->flags & HI_FLAG_PREFILL_2CTA);
-    if (!mma && !pair) {  // head groups in one launch (grid.y)
-        if (c->flags & HI_FLAG_PREFILL_TC1) return hi::launch_prefill_tc1(p, c->d, c->s_comp);
+    if (!mma && !pair && !(c->flags & HI_FLAG_PREFILL_TC1))  // the product kernel: head maps in one launch (grid.y)
         return hi::launch_prefill_tc(p, c->d, c->s_comp);
-    }
-    for (int h = 0; h < std::max(1, p.n_heads); ++h) {  // single-head kernels: one launch per head of the group
+    for (int h = 0; h < std::max(1, p.n_heads); ++h) {  // single-head launches of the comparison kernels
         hi::PrefillParams q1 = p;
         q1.n_heads = 1;
-        q1.q = p.q + static_cast<int64_t>(h) * p.g * c->d;
-        q1.out = p.out + static_cast<int64_t>(h) * p.g * c->d;
-        q1.k = p.k + h * p.kv_head_stride;
-        q1.v = p.v + h * p.kv_head_stride;
+        q1.q = p.q + static_cast<int64_t>(p.head_q[h]) * p.g * c->d;
+        q1.out = p.out + static_cast<int64_t>(p.head_q[h]) * p.g * c->d;
+        q1.k = p.k + p.head_kv[h] * p.kv_head_stride;
+        q1.v = p.v + p.head_kv[h] * p.kv_head_stride;
         q1.o_acc = p.o_acc + h * p.state_rows * c->d;
         q1.m_acc = p.m_acc + h * p.state_rows;
         q1.l_acc = p.l_acc + h * p.state_rows;
-        const cudaError_t e = mma ? hi::launch_prefill_mma(q1, c->d, c->s_comp) : hi::launch_prefill_tc2(q1, c->d, c->s_comp);
+        hi::set_identity_heads(q1, 1);
+        const cudaError_t e = mma ? hi::launch_prefill_mma(q1, c->d, c->s_comp)
+                              : pair ? hi::launch_prefill_tc2(q1, c->d, c->s_comp)
+                                     : hi::launch_prefill_tc1(q1, c->d, c->s_comp);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -297,9 +331,10 @@ hi_status check_call(hi_ctx* c, int layer) {
     return HI_OK;
 }
 
-// Enqueue the H2D of history block [k0, k0+nk) of kv heads [h0, h0+nh) of `layer` into the next slot;
-// the compute stream is made to wait for it.  Returns the slot index through *slot_out.
-hi_status stage_block(hi_ctx* c, int layer, int h0, int nh, int64_t k0, int64_t nk, int* slot_out) {
+// Enqueue the H2D of history block [k0, k0+nk) of the kv heads `heads` of `layer` into the next slot (head
+// heads[gh] at slot position gh); the compute stream is made to wait for it.  Returns the slot through *slot_out.
+hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64_t k0, int64_t nk, int* slot_out) {
+    const int nh = static_cast<int>(heads.size());
     const int s = c->next_slot;
     c->next_slot = (c->next_slot + 1) % c->n_slots;
     Slot& sl = c->slots[s];
@@ -310,8 +345,8 @@ hi_status stage_block(hi_ctx* c, int layer, int h0, int nh, int64_t k0, int64_t 
     }
     const size_t bytes = static_cast<size_t>(nk) * c->d * 2;
     for (int gh = 0; gh < nh; ++gh) {
-        HI_CK(c, cudaMemcpyAsync(c->slot_k(s, gh), c->host_k(layer, h0 + gh, k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
-        HI_CK(c, cudaMemcpyAsync(c->slot_v(s, gh), c->host_v(layer, h0 + gh, k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
+        HI_CK(c, cudaMemcpyAsync(c->slot_k(s, gh), c->host_k(layer, heads[gh], k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
+        HI_CK(c, cudaMemcpyAsync(c->slot_v(s, gh), c->host_v(layer, heads[gh], k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
     }
     HI_CK(c, cudaEventRecord(sl.ready, c->s_h2d));
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, sl.ready, 0));  // RAW: block landed
@@ -427,6 +462,25 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
                        "head_group = -1 or >= 1 dividing kv_heads/world)";
         return HI_EINVAL;
     }
+    if (kv_heads / world > hi::MAX_LAUNCH_HEADS) {
+        g_init_error = "kv_heads/world must be <= 64";
+        return HI_EINVAL;
+    }
+    // NEXT-3 duo streaming heads (reading R18): labels of this shard's kv heads
+    int n_stream_lab = 0;
+    if (o.streaming_heads)
+        for (int l = 0; l < layers; ++l)
+            for (int h = 0; h < kv_heads / world; ++h)
+                n_stream_lab += o.streaming_heads[static_cast<size_t>(l) * kv_heads + rank * (kv_heads / world) + h] != 0;
+    if (o.duo_sink == 0) o.duo_sink = 64;
+    if (o.duo_sink < 0) o.duo_sink = 0;
+    if (o.duo_window == 0) o.duo_window = 256;
+    if (n_stream_lab > 0 &&
+        (o.duo_window < 1 || o.duo_window > (1 << 20) || o.duo_sink > (1 << 20) ||
+         (o.flags & (HI_FLAG_MMA_SYNC_PREFILL | HI_FLAG_PREFILL_2CTA | HI_FLAG_PREFILL_TC1)))) {
+        g_init_error = "streaming heads need duo_window in [1, 2^20], duo_sink <= 2^20 and the default prefill kernel";
+        return HI_EINVAL;
+    }
 
     hi_ctx* c = new hi_ctx();
     c->L = layers; c->Hq = q_heads; c->Hkv = kv_heads; c->d = head_dim; c->chunk = chunk;
@@ -477,16 +531,50 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     c->group = o.head_group;
     c->slot_bytes = head_slot_bytes * c->group;
 
-    // (a) residency (NEXT-1, Alg. 1 H_on): the first n_res (layer, kv head) pairs keep their KV in HBM
+    // head classes: retrieval pairs numbered layer-major (cidx), streaming pairs -1 (NEXT-3)
     const int n_pairs = layers * c->Hkv_loc;
+    c->cidx.assign(n_pairs, -1);
+    for (int l = 0; l < layers; ++l)
+        for (int h = 0; h < c->Hkv_loc; ++h) {
+            const bool str = o.streaming_heads &&
+                             o.streaming_heads[static_cast<size_t>(l) * kv_heads + rank * c->Hkv_loc + h] != 0;
+            if (!str) c->cidx[static_cast<size_t>(l) * c->Hkv_loc + h] = c->n_retr++;
+        }
+    c->n_stream = n_pairs - c->n_retr;
+    if (c->n_stream > 0) {
+        c->duo_sink = o.duo_sink;
+        c->duo_win = o.duo_window;
+        c->duo_ring = o.duo_window;  // history needs the last duo_window - 1 rows; the ring holds duo_window
+        c->duo_rows = c->duo_sink + c->duo_ring;
+        c->duo_bytes = static_cast<size_t>(n_pairs) * c->duo_head_elems() * 2;  // indexed by (layer, head)
+        if (cudaMalloc(reinterpret_cast<void**>(&c->d_duo), c->duo_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return bail(HI_ENOMEM_DEV, "cudaMalloc of the streaming-head KV buffers failed");
+        }
+    }
+    // (a) residency (NEXT-1, Alg. 1 H_on): the first n_res retrieval pairs keep their KV in HBM
     const size_t pair_bytes = 2 * static_cast<size_t>(max_ctx) * head_dim * 2;
     if (o.resident_kv_heads == HI_RESIDENT_AUTO) {
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); free_b = 0; }
         const size_t reserve = (size_t(12) << 30) + c->slot_bytes * c->n_slots;  // workspaces + caller tensors
-        c->n_res = free_b > reserve ? static_cast<int>(std::min<size_t>(n_pairs, (free_b - reserve) / pair_bytes)) : 0;
+        c->n_res = free_b > reserve ? static_cast<int>(std::min<size_t>(c->n_retr, (free_b - reserve) / pair_bytes)) : 0;
     } else {
-        c->n_res = std::min(o.resident_kv_heads, n_pairs);
+        c->n_res = std::min(o.resident_kv_heads, c->n_retr);
+    }
+    // per-layer schedules: resident retrieval heads, offload units of up to `group` heads, streaming heads
+    c->res_heads.assign(layers, {});
+    c->str_heads.assign(layers, {});
+    c->off_units.assign(layers, {});
+    for (int l = 0; l < layers; ++l) {
+        std::vector<int> off;
+        for (int h = 0; h < c->Hkv_loc; ++h) {
+            if (c->streaming(l, h)) c->str_heads[l].push_back(h);
+            else if (c->resident(l, h)) c->res_heads[l].push_back(h);
+            else off.push_back(h);
+        }
+        for (size_t i = 0; i < off.size(); i += c->group)
+            c->off_units[l].emplace_back(off.begin() + i, off.begin() + std::min(off.size(), i + c->group));
     }
     c->res_bytes = static_cast<size_t>(c->n_res) * pair_bytes;
     if (c->n_res > 0 && cudaMalloc(reinterpret_cast<void**>(&c->d_res), c->res_bytes) != cudaSuccess) {
@@ -494,7 +582,7 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
         return bail(HI_ENOMEM_DEV, "cudaMalloc of the resident KV cache failed");
     }
     // (a) host store for the offloaded pairs
-    c->host_bytes = static_cast<size_t>(n_pairs - c->n_res) * pair_bytes;
+    c->host_bytes = static_cast<size_t>(c->n_retr - c->n_res) * pair_bytes;
     hi_status hs = alloc_host_store(c, o.numa_policy, o.numa_node);
     if (hs != HI_OK) return bail(hs, "");
 
@@ -509,6 +597,8 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     const int64_t max_blocks = (max_ctx + st - 1) / st;
     c->max_parts = static_cast<int>(std::max<int64_t>(max_blocks * decode_parts_for_block(std::min<int64_t>(st, max_ctx)),
                                                      decode_parts_for_block(max_ctx)) + 8);
+    if (c->n_stream > 0)  // sink segment + up to two ring runs, each split into >= 64-key parts
+        c->max_parts = std::max<int>(c->max_parts, static_cast<int>((c->duo_sink + 63) / 64 + (c->duo_ring + 63) / 64 + 8));
     const size_t pack_b = static_cast<size_t>(c->Hkv_loc) * 2 * chunk * head_dim * 2;
     const size_t oacc_b = rows * head_dim * 4 * c->group, ml_b = rows * 4 * c->group;
     const size_t parts_b = static_cast<size_t>(c->Hkv_loc) * c->max_parts * g * (head_dim + 4) * 4;
@@ -569,10 +659,12 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     // history H2D of this layer must see every earlier write-back of its rows (RAW via host DRAM)
     HI_CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_layer_d2h[layer], 0));
     // write-back (Alg. 1 line 11): D2H of the chunk's rows [s, s+n) of every offloaded local kv head;
-    // resident heads (Alg. 1 line 8 "Update GPU KV cache") append on the compute stream instead
+    // resident heads (Alg. 1 line 8 "Update GPU KV cache") append on the compute stream instead; streaming
+    // heads (NEXT-3) keep only their sink + window on the GPU (appended after their attention below)
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
     const size_t row_bytes = static_cast<size_t>(d) * 2;
     for (int h = 0; h < Hkv; ++h) {
+        if (c->streaming(layer, h)) continue;
         const __nv_bfloat16* pk = c->d_pack + (static_cast<size_t>(h) * 2 + 0) * n * d;
         const __nv_bfloat16* pv = c->d_pack + (static_cast<size_t>(h) * 2 + 1) * n * d;
         if (c->resident(layer, h)) {
@@ -587,91 +679,155 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     HI_CK(c, cudaEventRecord(c->ev_pack_free, c->s_d2h));
     HI_CK(c, cudaEventRecord(c->ev_layer_d2h[layer], c->s_d2h));
 
-    // attention, one kv head at a time (Alg. 1 line 5 loop)
+    // attention, one unit of kv heads at a time (Alg. 1 line 5 loop; NEXT-2 head groups when group > 1)
     const int64_t nb = (s + c->slot_tokens - 1) / c->slot_tokens;
-    hi::PrefillParams p{};
-    p.q_tok_stride = static_cast<int64_t>(c->Hq_loc) * d;
-    p.o_tok_stride = p.q_tok_stride;
-    p.n_q = n;
-    p.q_pos0 = s;
-    p.g = g;
-    p.scale_log2 = c->scale_log2;
-    p.o_acc = c->d_oacc;
-    p.m_acc = c->d_macc;
-    p.l_acc = c->d_lacc;
-    p.state_rows = static_cast<int64_t>(c->chunk) * g;
-    const int r_l = c->resident_heads_of_layer(layer);
-    // H_on heads of this layer (NEXT-1): chunk segment + the whole history straight from the HBM cache
-    for (int h = 0; h < r_l; ++h) {
-        p.n_heads = 1;
-        p.q = static_cast<const __nv_bfloat16*>(Q) + static_cast<size_t>(h) * g * d;
-        p.out = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(h) * g * d;
-        p.k = c->d_pack + (static_cast<size_t>(h) * 2 + 0) * n * d;
-        p.v = c->d_pack + (static_cast<size_t>(h) * 2 + 1) * n * d;
-        p.kv_row_stride = d;
-        p.n_k = n;
-        p.k_pos0 = s;
-        p.flags = hi::PF_FIRST | hi::PF_CAUSAL | (s == 0 ? hi::PF_LAST : 0);
-        {
-            LaunchTimer tm(c);
-            HI_CK(c, launch_prefill(c, p));
-            tm.done(4.0 * d * g * (static_cast<double>(n) * (n + 1) / 2.0), true);
-        }
+    hi::PrefillParams base{};
+    base.q = static_cast<const __nv_bfloat16*>(Q);
+    base.out = static_cast<__nv_bfloat16*>(out);
+    base.q_tok_stride = static_cast<int64_t>(c->Hq_loc) * d;
+    base.o_tok_stride = base.q_tok_stride;
+    base.n_q = n;
+    base.q_pos0 = s;
+    base.g = g;
+    base.scale_log2 = c->scale_log2;
+    base.o_acc = c->d_oacc;
+    base.m_acc = c->d_macc;
+    base.l_acc = c->d_lacc;
+    base.state_rows = static_cast<int64_t>(c->chunk) * g;
+    base.q_span = Hkv;
+    const bool timing = c->flags & HI_FLAG_TIMING;
+    // one launch over segment keys [k_pos0, k_pos0 + n_k) for the unit's heads
+    auto run = [&](hi::PrefillParams& p, int flags) -> hi_status {
+        p.flags = flags;
+        LaunchTimer tm(c);
+        HI_CK(c, launch_prefill(c, p));
+        if (timing)
+            tm.done(4.0 * d * g * p.n_heads * seg_pairs(s, n, p.k_pos0, p.n_k, flags & hi::PF_CAUSAL, p.win), true);
         ++c->launches;
-        if (s > 0) {
-            p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, h, 0));
-            p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, h, 0));
-            p.n_k = static_cast<int>(s);
-            p.k_pos0 = 0;
-            p.flags = hi::PF_LAST;
-            LaunchTimer tm(c);
-            HI_CK(c, launch_prefill(c, p));
-            tm.done(4.0 * d * g * static_cast<double>(n) * static_cast<double>(s), true);
-            ++c->launches;
-        }
-    }
-    // offloaded heads, `group` at a time (Alg. 1 line 5 loop; NEXT-2 head groups when group > 1)
-    for (int h0 = r_l; h0 < Hkv; h0 += c->group) {
-        const int nh = std::min(c->group, Hkv - h0);
-        p.n_heads = nh;
-        p.q = static_cast<const __nv_bfloat16*>(Q) + static_cast<size_t>(h0) * g * d;
-        p.out = static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(h0) * g * d;
-        // the chunk's own keys first: causal, no transfer needed (pack buffer: [h][K|V][n][d])
-        p.k = c->d_pack + (static_cast<size_t>(h0) * 2 + 0) * n * d;
-        p.v = c->d_pack + (static_cast<size_t>(h0) * 2 + 1) * n * d;
+        return HI_OK;
+    };
+    // the chunk's own keys [s + r0, s + n) from the pack buffer ([h][K|V][n][d]); kv coordinate = the real head
+    auto chunk_seg = [&](hi::PrefillParams& p, const std::vector<int>& unit, int r0) {
+        p.k = c->d_pack + static_cast<size_t>(r0) * d;
+        p.v = c->d_pack + static_cast<size_t>(n) * d + static_cast<size_t>(r0) * d;
         p.kv_row_stride = d;
         p.kv_head_stride = static_cast<int64_t>(2) * n * d;
-        p.n_k = n;
-        p.k_pos0 = s;
-        p.flags = hi::PF_FIRST | hi::PF_CAUSAL | (s == 0 ? hi::PF_LAST : 0);
-        {
-            LaunchTimer tm(c);
-            HI_CK(c, launch_prefill(c, p));
-            tm.done(4.0 * d * g * nh * (static_cast<double>(n) * (n + 1) / 2.0), true);
+        for (size_t y = 0; y < unit.size(); ++y) p.head_kv[y] = static_cast<int16_t>(unit[y]);
+        p.kv_span = Hkv;
+        p.n_k = n - r0;
+        p.k_pos0 = s + r0;
+    };
+    auto start_unit = [&](const std::vector<int>& unit) {
+        hi::PrefillParams p = base;
+        p.n_heads = static_cast<int>(unit.size());
+        for (size_t y = 0; y < unit.size(); ++y) p.head_q[y] = static_cast<int16_t>(unit[y]);
+        return p;
+    };
+    auto units_of = [&](const std::vector<int>& heads) {
+        std::vector<std::vector<int>> u;
+        for (size_t i = 0; i < heads.size(); i += c->group)
+            u.emplace_back(heads.begin() + i, heads.begin() + std::min(heads.size(), i + c->group));
+        return u;
+    };
+    // H_on heads of this layer (NEXT-1): chunk segment + the whole history straight from the HBM cache
+    // (consecutive resident pairs are 2*max_ctx rows apart)
+    for (const auto& unit : units_of(c->res_heads[layer])) {
+        hi::PrefillParams p = start_unit(unit);
+        chunk_seg(p, unit, 0);
+        if ((st = run(p, hi::PF_FIRST | hi::PF_CAUSAL | (s == 0 ? hi::PF_LAST : 0))) != HI_OK) return st;
+        if (s > 0) {
+            p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, unit[0], 0));
+            p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, unit[0], 0));
+            p.kv_head_stride = 2 * c->max_ctx * d;
+            for (size_t y = 0; y < unit.size(); ++y) p.head_kv[y] = static_cast<int16_t>(y);
+            p.kv_span = static_cast<int>(unit.size());
+            p.n_k = static_cast<int>(s);
+            p.k_pos0 = 0;
+            if ((st = run(p, hi::PF_LAST)) != HI_OK) return st;
         }
-        ++c->launches;
-        // history blocks [0, s) of the group's heads through the staging slots (Alg. 1 line 10 prefetch)
+    }
+    // offloaded heads, `group` at a time
+    for (const auto& unit : c->off_units[layer]) {
+        hi::PrefillParams p = start_unit(unit);
+        // the chunk's own keys first: causal, no transfer needed
+        chunk_seg(p, unit, 0);
+        if ((st = run(p, hi::PF_FIRST | hi::PF_CAUSAL | (s == 0 ? hi::PF_LAST : 0))) != HI_OK) return st;
+        // history blocks [0, s) of the unit's heads through the staging slots (Alg. 1 line 10 prefetch)
         for (int64_t b = 0; b < nb; ++b) {
             const int64_t k0 = b * c->slot_tokens;
             const int64_t nk = std::min<int64_t>(c->slot_tokens, s - k0);
             int slot = 0;
-            st = stage_block(c, layer, h0, nh, k0, nk, &slot);
+            st = stage_block(c, layer, unit, k0, nk, &slot);
             if (st != HI_OK) return st;
             p.k = reinterpret_cast<const __nv_bfloat16*>(c->slot_k(slot));
             p.v = reinterpret_cast<const __nv_bfloat16*>(c->slot_v(slot));
             p.kv_head_stride = static_cast<int64_t>(c->slot_head_bytes() / 2);
+            for (size_t y = 0; y < unit.size(); ++y) p.head_kv[y] = static_cast<int16_t>(y);
+            p.kv_span = static_cast<int>(unit.size());
             p.n_k = static_cast<int>(nk);
             p.k_pos0 = k0;
-            p.flags = (b == nb - 1) ? hi::PF_LAST : 0;
-            {
-                LaunchTimer tm(c);
-                HI_CK(c, launch_prefill(c, p));
-                tm.done(4.0 * d * g * nh * static_cast<double>(n) * static_cast<double>(nk), true);
-            }
-            ++c->launches;
+            if ((st = run(p, (b == nb - 1) ? hi::PF_LAST : 0)) != HI_OK) return st;
             st = release_slot(c, slot);
             if (st != HI_OK) return st;
         }
+    }
+    // duo streaming heads (NEXT-3, reading R18): row p attends keys i <= p with i < duo_sink or i > p - duo_win.
+    // Segments: the chunk's sink keys, the chunk's windowed keys, the history sink, the history window (ring
+    // runs) -- each wholly sink or wholly non-sink, so the kernel applies the band to non-sink segments only.
+    if (!c->str_heads[layer].empty()) {
+        const int64_t ns = c->duo_sink;
+        for (const auto& unit : units_of(c->str_heads[layer])) {
+            hi::PrefillParams p = start_unit(unit);
+            struct Seg { int64_t row0_or_r0; int64_t n_k, k_pos0; bool chunk, causal; int win; };
+            std::vector<Seg> segs;
+            if (s < ns) segs.push_back({0, std::min<int64_t>(n, ns - s), s, true, true, 0});
+            const int64_t c0 = std::max<int64_t>(s, ns) - s;
+            if (c0 < n) segs.push_back({c0, n - c0, s + c0, true, true, c->duo_win});
+            if (s > 0 && ns > 0) segs.push_back({0, std::min<int64_t>(ns, s), 0, false, false, 0});
+            for (int64_t pos = std::max<int64_t>(ns, s - c->duo_win + 1); pos < s;) {
+                const int64_t row = c->duo_row(pos);
+                const int64_t len = std::min<int64_t>(s - pos, c->duo_rows - row);
+                segs.push_back({row, len, pos, false, false, c->duo_win});
+                pos += len;
+            }
+            for (size_t i = 0; i < segs.size(); ++i) {
+                const Seg& sg = segs[i];
+                if (sg.chunk) {
+                    chunk_seg(p, unit, static_cast<int>(sg.row0_or_r0));
+                    p.n_k = static_cast<int>(sg.n_k);
+                } else {
+                    p.k = c->duo_k(layer, 0, sg.row0_or_r0);
+                    p.v = p.k + c->duo_rows * d;
+                    p.kv_row_stride = d;
+                    p.kv_head_stride = static_cast<int64_t>(c->duo_head_elems());
+                    for (size_t y = 0; y < unit.size(); ++y) p.head_kv[y] = static_cast<int16_t>(unit[y]);
+                    p.kv_span = Hkv;
+                    p.n_k = static_cast<int>(sg.n_k);
+                    p.k_pos0 = sg.k_pos0;
+                }
+                p.win = sg.win;
+                const int fl = (i == 0 ? hi::PF_FIRST : 0) | (i + 1 == segs.size() ? hi::PF_LAST : 0) |
+                               (sg.causal ? hi::PF_CAUSAL : 0);
+                if ((st = run(p, fl)) != HI_OK) return st;
+            }
+        }
+        // then the chunk's surviving rows go into the sink / ring (after every read of the old window)
+        hi::DuoAppendParams ap{};
+        ap.src_k = c->d_pack;
+        ap.src_v = c->d_pack + static_cast<size_t>(n) * d;
+        ap.src_head_stride = static_cast<int64_t>(2) * n * d;
+        ap.src_row_stride = d;
+        ap.dst = c->duo_k(layer, 0, 0);
+        ap.dst_head_stride = static_cast<int64_t>(c->duo_head_elems());
+        ap.dst_v_off = c->duo_rows * d;
+        ap.pos0 = s;
+        ap.n = n;
+        ap.n_sink = c->duo_sink;
+        ap.ring = c->duo_ring;
+        ap.n_heads = static_cast<int>(c->str_heads[layer].size());
+        for (int y = 0; y < ap.n_heads; ++y) ap.heads[y] = static_cast<int16_t>(c->str_heads[layer][y]);
+        HI_CK(c, hi::launch_duo_append(ap, d, c->s_comp));
+        ++c->launches;
     }
     st = finish_call(c, cs);
     if (st != HI_OK) return st;
@@ -700,9 +856,10 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     HI_CK(c, cudaMemcpyAsync(vn, v, Hkv * row_bytes, cudaMemcpyDeviceToDevice, c->s_comp));
     HI_CK(c, cudaEventRecord(c->ev_packed, c->s_comp));
     HI_CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_layer_d2h[layer], 0));
-    // append (Alg. 1 line 26 "Async Update CPU KV cache"): host row s of every local kv head
+    // append (Alg. 1 line 26 "Async Update CPU KV cache"): host row s of every offloaded local kv head
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
     for (int h = 0; h < Hkv; ++h) {
+        if (c->streaming(layer, h)) continue;  // NEXT-3: sink / ring append below
         if (c->resident(layer, h)) {  // H_on: append in HBM (compute stream; read by later calls only)
             HI_CK(c, cudaMemcpyAsync(c->dev_k(layer, h, s), kn + static_cast<size_t>(h) * d, row_bytes,
                                      cudaMemcpyDeviceToDevice, c->s_comp));
@@ -719,70 +876,111 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     HI_CK(c, cudaEventRecord(c->ev_kvnew_free[layer], c->s_d2h));
     HI_CK(c, cudaEventRecord(c->ev_layer_d2h[layer], c->s_d2h));
 
-    // history: per kv head, blocks through the slots -> split-K partial records
-    const int64_t nb = (s + c->slot_tokens - 1) / c->slot_tokens;
-    int n_parts_off = 0, n_parts_res = 0;
-    const int r_l = c->resident_heads_of_layer(layer);
-    if (r_l > 0 && s > 0) {  // H_on heads of this layer: ONE split-K launch over [0, s) of all of them, in HBM
-        hi::DecodePartialParams p{};
+    // history -> split-K partial records, per local kv head h at parts[h][0 .. n_parts[h])
+    hi::DecodeCombineParams cp{};
+    const int64_t rec = static_cast<int64_t>(g) * (d + 4);
+    auto partial = [&](hi::DecodePartialParams& p, const std::vector<int>& heads, int64_t nk, int pofs) -> int {
         p.q = static_cast<const __nv_bfloat16*>(q);
-        p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, 0, 0));
-        p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, 0, 0));
-        p.n_k = static_cast<int>(s);
-        p.split_len = decode_split_len(s, r_l);
+        p.n_k = static_cast<int>(nk);
+        p.split_len = decode_split_len(nk, static_cast<int>(heads.size()));
         p.scale_log2 = c->scale_log2;
-        p.parts = c->d_parts;
-        p.kv_head_stride = 2 * c->max_ctx * d;              // pairs are [K | V] blocks of max_ctx rows
+        p.parts = c->d_parts + pofs * rec;
         p.q_head_stride = static_cast<int64_t>(g) * d;
-        p.parts_head_stride = static_cast<int64_t>(c->max_parts) * g * (d + 4);
-        n_parts_res = static_cast<int>((s + p.split_len - 1) / p.split_len);
+        p.parts_head_stride = static_cast<int64_t>(c->max_parts) * rec;
+        for (size_t y = 0; y < heads.size(); ++y) p.head[y] = static_cast<int16_t>(heads[y]);
+        return static_cast<int>((nk + p.split_len - 1) / p.split_len);
+    };
+    auto launch = [&](const hi::DecodePartialParams& p, int nsp, int nh, int64_t nk) -> hi_status {
         LaunchTimer tm(c);
-        HI_CK(c, hi::launch_decode_partial(p, d, g, n_parts_res, r_l, c->s_comp));
-        tm.done(4.0 * d * static_cast<double>(s) * r_l, false);
+        HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, nh, c->s_comp));
+        tm.done(4.0 * d * static_cast<double>(nk) * nh, false);
         ++c->launches;
+        return HI_OK;
+    };
+    const auto& R = c->res_heads[layer];
+    if (!R.empty() && s > 0) {  // H_on heads of this layer: ONE split-K launch over [0, s) of all of them, in HBM
+        hi::DecodePartialParams p{};
+        const int nsp = partial(p, R, s, 0);
+        p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, R[0], 0));
+        p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, R[0], 0));
+        p.kv_head_stride = 2 * c->max_ctx * d;  // consecutive resident pairs are [K | V] blocks of max_ctx rows
+        for (size_t y = 0; y < R.size(); ++y) p.kvc[y] = static_cast<int16_t>(y);
+        p.kv_span = static_cast<int>(R.size());
+        if ((st = launch(p, nsp, static_cast<int>(R.size()), s)) != HI_OK) return st;
+        for (int h : R) cp.n_parts[h] = static_cast<int16_t>(nsp);
     }
-    for (int h0 = r_l; h0 < Hkv; h0 += c->group) {
-        const int nh = std::min(c->group, Hkv - h0);
+    const int64_t nb = (s + c->slot_tokens - 1) / c->slot_tokens;
+    for (const auto& unit : c->off_units[layer]) {
+        const int nh = static_cast<int>(unit.size());
         int pofs = 0;
         for (int64_t b = 0; b < nb; ++b) {
             const int64_t k0 = b * c->slot_tokens;
             const int64_t nk = std::min<int64_t>(c->slot_tokens, s - k0);
             int slot = 0;
-            st = stage_block(c, layer, h0, nh, k0, nk, &slot);
+            st = stage_block(c, layer, unit, k0, nk, &slot);
             if (st != HI_OK) return st;
             hi::DecodePartialParams p{};
-            p.q = static_cast<const __nv_bfloat16*>(q) + static_cast<size_t>(h0) * g * d;
+            const int nsp = partial(p, unit, nk, pofs);
             p.k = reinterpret_cast<const __nv_bfloat16*>(c->slot_k(slot));
             p.v = reinterpret_cast<const __nv_bfloat16*>(c->slot_v(slot));
-            p.n_k = static_cast<int>(nk);
-            p.split_len = decode_split_len(nk, nh);
-            p.scale_log2 = c->scale_log2;
-            p.parts = c->d_parts + (static_cast<size_t>(h0) * c->max_parts + pofs) * g * (d + 4);
             p.kv_head_stride = static_cast<int64_t>(c->slot_head_bytes() / 2);
-            p.q_head_stride = static_cast<int64_t>(g) * d;
-            p.parts_head_stride = static_cast<int64_t>(c->max_parts) * g * (d + 4);
-            const int nsp = static_cast<int>((nk + p.split_len - 1) / p.split_len);
-            {
-                LaunchTimer tm(c);
-                HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, nh, c->s_comp));
-                tm.done(4.0 * d * static_cast<double>(nk) * nh, false);
-            }
-            ++c->launches;
+            for (int y = 0; y < nh; ++y) p.kvc[y] = static_cast<int16_t>(y);
+            p.kv_span = nh;
+            if ((st = launch(p, nsp, nh, nk)) != HI_OK) return st;
             pofs += nsp;
             st = release_slot(c, slot);
             if (st != HI_OK) return st;
         }
-        n_parts_off = pofs;
+        for (int h : unit) cp.n_parts[h] = static_cast<int16_t>(pofs);
     }
-    hi::DecodeCombineParams cp{};
+    const auto& S = c->str_heads[layer];
+    if (!S.empty()) {  // NEXT-3 streaming heads: the sink rows and the window's ring runs, all heads per launch
+        const int nh = static_cast<int>(S.size());
+        int pofs = 0;
+        auto seg = [&](int64_t row, int64_t nk) -> hi_status {
+            hi::DecodePartialParams p{};
+            const int nsp = partial(p, S, nk, pofs);
+            p.k = c->duo_k(layer, 0, row);
+            p.v = p.k + c->duo_rows * d;
+            p.kv_head_stride = static_cast<int64_t>(c->duo_head_elems());
+            for (int y = 0; y < nh; ++y) p.kvc[y] = static_cast<int16_t>(S[y]);
+            p.kv_span = Hkv;
+            hi_status e = launch(p, nsp, nh, nk);
+            pofs += nsp;
+            return e;
+        };
+        if (s > 0 && c->duo_sink > 0)
+            if ((st = seg(0, std::min<int64_t>(c->duo_sink, s))) != HI_OK) return st;
+        for (int64_t pos = std::max<int64_t>(c->duo_sink, s - c->duo_win + 1); pos < s;) {
+            const int64_t row = c->duo_row(pos);
+            const int64_t len = std::min<int64_t>(s - pos, c->duo_rows - row);
+            if ((st = seg(row, len)) != HI_OK) return st;
+            pos += len;
+        }
+        for (int h : S) cp.n_parts[h] = static_cast<int16_t>(pofs);
+        // the new token's row joins the sink / ring (its ring row is not one the window above read)
+        hi::DuoAppendParams ap{};
+        ap.src_k = kn;
+        ap.src_v = vn;
+        ap.src_head_stride = d;
+        ap.src_row_stride = 0;
+        ap.dst = c->duo_k(layer, 0, 0);
+        ap.dst_head_stride = static_cast<int64_t>(c->duo_head_elems());
+        ap.dst_v_off = c->duo_rows * d;
+        ap.pos0 = s;
+        ap.n = 1;
+        ap.n_sink = c->duo_sink;
+        ap.ring = c->duo_ring;
+        ap.n_heads = nh;
+        for (int y = 0; y < nh; ++y) ap.heads[y] = static_cast<int16_t>(S[y]);
+        HI_CK(c, hi::launch_duo_append(ap, d, c->s_comp));
+        ++c->launches;
+    }
     cp.q = static_cast<const __nv_bfloat16*>(q);
     cp.k_new = kn;
     cp.v_new = vn;
     cp.parts = c->d_parts;
     cp.max_parts = c->max_parts;
-    cp.n_parts = n_parts_off;
-    cp.n_parts_lo = n_parts_res;
-    cp.h_lo = c->resident_heads_of_layer(layer);
     cp.g = g;
     cp.scale_log2 = c->scale_log2;
     cp.out = static_cast<__nv_bfloat16*>(out);
@@ -810,6 +1008,22 @@ hi_status hi_read_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, v
     if (st != HI_OK) return st;
     if (h < 0 || h >= c->Hkv_loc || pos < 0 || n < 0 || pos + n > c->max_ctx || (n > 0 && (!k_dst || !v_dst)))
         return set_err(c, HI_ESHAPE, "bad host KV range");
+    if (c->streaming(layer, h)) {  // NEXT-3: only the sink rows and the last duo_win rows below seq_len exist
+        const int64_t sl = c->seq_len[layer];
+        for (int64_t p = pos; p < pos + n; ++p)
+            if (p >= sl || (p >= c->duo_sink && p < sl - c->duo_win))
+                return set_err(c, HI_ESTATE, "streaming head: row not held (only sink + recent window)");
+        st = hi_synchronize(c);
+        if (st != HI_OK) return st;
+        for (int64_t p = pos; p < pos + n; ++p) {
+            const int64_t r = c->duo_row(p);
+            uint8_t* kd = static_cast<uint8_t*>(k_dst) + (p - pos) * c->d * 2;
+            uint8_t* vd = static_cast<uint8_t*>(v_dst) + (p - pos) * c->d * 2;
+            HI_CK(c, cudaMemcpy(kd, c->duo_k(layer, h, r), c->d * 2, cudaMemcpyDeviceToHost));
+            HI_CK(c, cudaMemcpy(vd, c->duo_k(layer, h, r) + c->duo_rows * c->d, c->d * 2, cudaMemcpyDeviceToHost));
+        }
+        return HI_OK;
+    }
     if (c->resident(layer, h)) {
         st = hi_synchronize(c);
         if (st != HI_OK) return st;
@@ -832,6 +1046,19 @@ hi_status hi_write_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, 
     st = hi_synchronize(c);
     if (st != HI_OK) return st;
     const size_t bytes = static_cast<size_t>(n) * c->d * 2;
+    if (c->streaming(layer, h)) {  // NEXT-3: sink rows, then the last duo_ring rows of the range into the ring
+        const cudaMemcpyKind kind = from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        const int64_t lo_ring = std::max<int64_t>(c->duo_sink, pos + n - c->duo_ring);
+        for (int64_t p = pos; p < pos + n; ++p) {
+            if (p >= c->duo_sink && p < lo_ring) continue;
+            const int64_t r = c->duo_row(p);
+            const uint8_t* ks = static_cast<const uint8_t*>(k_src) + (p - pos) * c->d * 2;
+            const uint8_t* vs = static_cast<const uint8_t*>(v_src) + (p - pos) * c->d * 2;
+            HI_CK(c, cudaMemcpy(c->duo_k(layer, h, r), ks, c->d * 2, kind));
+            HI_CK(c, cudaMemcpy(c->duo_k(layer, h, r) + c->duo_rows * c->d, vs, c->d * 2, kind));
+        }
+        return HI_OK;
+    }
     if (c->resident(layer, h)) {
         const cudaMemcpyKind kind = from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         HI_CK(c, cudaMemcpy(c->dev_k(layer, h, pos), k_src, bytes, kind));
@@ -890,6 +1117,8 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     o->resident_kv_heads = c->n_res;
     o->resident_bytes = static_cast<int64_t>(c->res_bytes);
     o->head_group = c->group;
+    o->streaming_kv_heads = c->n_stream;
+    o->streaming_bytes = static_cast<int64_t>(c->duo_bytes);
     o->numa_node = c->numa_node;
     o->n_slots = c->n_slots;
     o->slot_tokens = c->slot_tokens;

@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(DM_THREADS, 1)
                 mbar_expect_tx(bar_full(s), STAGE);  // OOB rows of the last chunk are zero-filled, still counted
 #pragma unroll
                 for (int c = 0; c < NB; ++c) {
-                    tma_load_3d(sbase + s * STAGE + c * DM_BOX, &tm_k, bar_full(s), c * 64, k0, blockIdx.y);
-                    tma_load_3d(sbase + s * STAGE + (NB + c) * DM_BOX, &tm_v, bar_full(s), c * 64, k0, blockIdx.y);
+                    tma_load_3d(sbase + s * STAGE + c * DM_BOX, &tm_k, bar_full(s), c * 64, k0, p.kvc[blockIdx.y]);
+                    tma_load_3d(sbase + s * STAGE + (NB + c) * DM_BOX, &tm_v, bar_full(s), c * 64, k0, p.kvc[blockIdx.y]);
                 }
             }
         }
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(DM_THREADS, 1)
     // ---------------- consumers ----------------
     const int gid = lane >> 2, tq = lane & 3;
     const bool row_live = gid < G;
-    const __nv_bfloat16* qg = p.q + blockIdx.y * p.q_head_stride;
+    const __nv_bfloat16* qg = p.q + p.head[blockIdx.y] * p.q_head_stride;
     // Q fragments (A operand, rows = q heads of the group, zero-padded to 16), all of D
     uint32_t qa[D / 16][2];  // {a0a1 (row gid, k 0-7 of the step), a4a5 (row gid, k 8-15)}; rows gid+8 are 0
 #pragma unroll
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(DM_THREADS, 1)
         }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(DM_CONSUMERS * 32) : "memory");
-    float* rec = p.parts + blockIdx.y * p.parts_head_stride + static_cast<int64_t>(blockIdx.x) * G * (D + 4);
+    float* rec = p.parts + p.head[blockIdx.y] * p.parts_head_stride + static_cast<int64_t>(blockIdx.x) * G * (D + 4);
     for (int idx = threadIdx.x; idx < G * D; idx += DM_CONSUMERS * 32) {
         const int j = idx / D, c = idx % D;
         float mx = -CUDART_INF_F;
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32) decode_combine_kernel(const Dec
         for (int off = 16; off > 0; off >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, off);
         if (lane == 0) s_x = prod * p.scale_log2;
     }
-    const int n_parts = h < p.h_lo ? p.n_parts_lo : p.n_parts;
+    const int n_parts = p.n_parts[h];
     const float* recs = p.parts + (static_cast<int64_t>(h) * p.max_parts * p.g + j) * (D + 4);
     const int64_t rstride = static_cast<int64_t>(p.g) * (D + 4);
     float mx = -CUDART_INF_F;
@@ -355,8 +355,8 @@ cudaError_t launch_partial_dg(const DecodePartialParams& p, int n_splits, int n_
         configured = true;
     }
     CUtensorMap tk, tv;
-    const int64_t hs = n_heads > 1 ? p.kv_head_stride : static_cast<int64_t>(p.n_k) * D;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k), static_cast<cuuint64_t>(n_heads)};
+    const int64_t hs = p.kv_span > 1 ? p.kv_head_stride : static_cast<int64_t>(p.n_k) * D;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k), static_cast<cuuint64_t>(p.kv_span)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(hs) * 2};
     const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(DM_CHUNK), 1};
     if (!make_tmap_bf16(&tk, p.k, 3, dims, strides, box) || !make_tmap_bf16(&tv, p.v, 3, dims, strides, box))
@@ -381,6 +381,7 @@ cudaError_t launch_partial_d(const DecodePartialParams& p, int g, int n_splits, 
 cudaError_t launch_decode_partial(const DecodePartialParams& p, int d, int g, int n_splits, int n_heads,
                                   cudaStream_t stream) {
     if (n_splits <= 0 || n_heads <= 0) return cudaSuccess;
+    if (n_heads > MAX_LAUNCH_HEADS || p.kv_span < 1) return cudaErrorInvalidValue;
     if (d == 64) return launch_partial_d<64>(p, g, n_splits, n_heads, stream);
     if (d == 128) return launch_partial_d<128>(p, g, n_splits, n_heads, stream);
     return cudaErrorInvalidValue;

@@ -30,7 +30,42 @@ __global__ void poison_kernel(uint4* p, int64_t n16) {
         p[i] = nan4;
 }
 
+// NEXT-3: new K/V rows of the streaming heads -> device sink rows / ring rows (DuoAppendParams).  Only the
+// rows that survive the call are written: p < n_sink (sink) or p >= pos0 + n - ring (the last `ring` rows).
+__global__ void duo_append_kernel(const DuoAppendParams p, int cpr /* 16-byte chunks per row */) {
+    const int64_t skip_lo = p.pos0 + p.n - p.ring;  // rows >= max(n_sink, skip_lo) stay in the ring
+    const int64_t total = static_cast<int64_t>(p.n_heads) * p.n * cpr;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % cpr);
+        const int64_t yt = i / cpr;
+        const int t = static_cast<int>(yt % p.n);
+        const int y = static_cast<int>(yt / p.n);
+        const int64_t pos = p.pos0 + t;
+        int64_t row;
+        if (pos < p.n_sink) row = pos;
+        else if (pos >= skip_lo) row = p.n_sink + (pos - p.n_sink) % p.ring;
+        else continue;
+        const int h = p.heads[y];
+        const int64_t so = h * p.src_head_stride + t * p.src_row_stride;
+        __nv_bfloat16* dk = p.dst + h * p.dst_head_stride + row * (cpr * 8);
+        reinterpret_cast<uint4*>(dk)[c] = reinterpret_cast<const uint4*>(p.src_k + so)[c];
+        reinterpret_cast<uint4*>(dk + p.dst_v_off)[c] = reinterpret_cast<const uint4*>(p.src_v + so)[c];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_duo_append(const DuoAppendParams& p, int d, cudaStream_t stream) {
+    const int cpr = d / 8;
+    const int64_t total = static_cast<int64_t>(p.n_heads) * p.n * cpr;
+    if (total == 0) return cudaSuccess;
+    if (p.ring < 1 || p.n_heads > MAX_LAUNCH_HEADS) return cudaErrorInvalidValue;
+    const int threads = 256;
+    const int64_t want = (total + threads - 1) / threads;
+    duo_append_kernel<<<static_cast<int>(want < 148 * 8 ? want : 148 * 8), threads, 0, stream>>>(p, cpr);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pack_kv(const __nv_bfloat16* k, const __nv_bfloat16* v, __nv_bfloat16* packed, int n, int hkv,
                            int d, cudaStream_t stream) {

@@ -163,13 +163,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int g = p.g;
     const int n_rows = p.n_q * g;
     const int row0 = blockIdx.x * (2 * BM);
-    const int hh = blockIdx.y;                 // kv head within the launch's head group
+    const int hh = blockIdx.y;                 // kv head within the launch's head group (state index)
+    const int hq = p.head_q[hh], hk = p.head_kv[hh];  // its q/out columns and k/v coordinate (head maps)
     float* const o_acc = p.o_acc + static_cast<int64_t>(hh) * p.state_rows * D;
     float* const m_acc = p.m_acc + static_cast<int64_t>(hh) * p.state_rows;
     float* const l_acc = p.l_acc + static_cast<int64_t>(hh) * p.state_rows;
     const bool first = p.flags & PF_FIRST, last = p.flags & PF_LAST, causal = p.flags & PF_CAUSAL;
     const int n_tiles = (row0 + BM < n_rows) ? 2 : 1;  // second Q tile may be empty at the tail
 
+    // duo streaming band (NEXT-3): key c visible to token t only if k_pos0+c > q_pos0+t-win.  The CTA skips
+    // the KV tiles wholly below the band of its first row: its loop covers tiles kt_lo .. (key base kb).
+    const bool band = p.win > 0;
+    int kt_lo = 0;
+    if (band) {
+        const int64_t c_lo = p.q_pos0 + row0 / g - p.win + 1 - p.k_pos0;  // first visible key of the first row
+        kt_lo = c_lo > 0 ? static_cast<int>((c_lo < p.n_k ? c_lo : static_cast<int64_t>(p.n_k)) / BN) : 0;
+    }
+    const int kb = kt_lo * BN;
     // keys of the segment visible to tile tt (causal: key c visible to token t iff k_pos0+c <= q_pos0+t)
     auto kt_count = [&](int tt) {
         const int r0 = row0 + tt * BM;
@@ -180,7 +190,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             e = lim < e ? lim : e;
         }
         e = e > 0 ? e : 0;
-        return static_cast<int>((e + BN - 1) / BN);
+        return max(0, static_cast<int>((e + BN - 1) / BN) - kt_lo);
     };
     const int n_kt0 = kt_count(0);
     const int n_kt1 = n_tiles == 2 ? kt_count(1) : 0;
@@ -229,17 +239,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_expect_tx(bar_q, n_tiles * (D / 64) * L::BOX);
             for (int tt = 0; tt < n_tiles; ++tt)
                 for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sbase + L::Q_OFF + (tt * (D / 64) + c) * L::BOX, &tm_q, bar_q, c * 64, hh * g,
+                    tma_load_3d(sbase + L::Q_OFF + (tt * (D / 64) + c) * L::BOX, &tm_q, bar_q, c * 64, hq * g,
                                 (row0 + tt * BM) / g);
             for (int i = 0; i < n_kt; ++i) {
                 const int s = i % NS;
                 if (i >= NS) mbar_wait(bar_e(s), ((i / NS) - 1) & 1);
                 mbar_expect_tx(bar_k(s), (D / 64) * L::BOX);
                 for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sbase + L::K_OFF + (s * (D / 64) + c) * L::BOX, &tm_k, bar_k(s), c * 64, i * BN, hh);
+                    tma_load_3d(sbase + L::K_OFF + (s * (D / 64) + c) * L::BOX, &tm_k, bar_k(s), c * 64, kb + i * BN, hk);
                 mbar_expect_tx(bar_v(s), (D / 64) * L::BOX);
                 for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, i * BN, hh);
+                    tma_load_3d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, kb + i * BN, hk);
             }
         } else if (warp == WARP_MMA && lane == 0 && n_kt > 0) {
             // ============================ MMA issuer ==============================
@@ -380,6 +390,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int64_t qpos = p.q_pos0 + t;
         const int nkt = tt == 0 ? n_kt0 : n_kt1;
         const int t_lo = (row0 + tt * BM) / g;
+        const int t_hi_tile = min(p.n_q - 1, (row0 + tt * BM + BM - 1) / g);
         const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
         const uint32_t t_s = tmem + tt * 256 + lane_addr;        // S / P columns of this row
         const uint32_t t_o = t_s + 128 + hf * HD;                // this thread's O columns
@@ -419,14 +430,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tmem_wait_ld();
                 HI_TR(ttr + 0, j);
                 // row max of the raw scores (scale > 0 commutes with max); masking where needed
-                const int key0 = j * BN + hf * HN;
-                const bool need_mask = (j * BN + BN > p.n_k) || (causal && p.k_pos0 + j * BN + BN - 1 > p.q_pos0 + t_lo);
+                const int key0 = kb + j * BN + hf * HN;
+                const int kt0 = kb + j * BN;  // first key of the tile
+                const bool need_mask = (kt0 + BN > p.n_k) || (causal && p.k_pos0 + kt0 + BN - 1 > p.q_pos0 + t_lo);
                 if (need_mask) {
                     const int64_t lim = causal ? qpos - p.k_pos0 : static_cast<int64_t>(p.n_k) - 1;
                     const int64_t lim2 = lim < p.n_k - 1 ? lim : static_cast<int64_t>(p.n_k) - 1;
 #pragma unroll
                     for (int i = 0; i < HN; ++i)
                         if (key0 + i > lim2) x[i] = __float_as_uint(-CUDART_INF_F);
+                }
+                // band lower edge: keys c <= qpos - win - k_pos0 fall out of the recent window
+                if (band && p.k_pos0 + kt0 <= p.q_pos0 + t_hi_tile - p.win) {
+                    const int64_t lo = qpos - p.win - p.k_pos0;
+#pragma unroll
+                    for (int i = 0; i < HN; ++i)
+                        if (key0 + i <= lo) x[i] = __float_as_uint(-CUDART_INF_F);
                 }
                 if constexpr (SPLIT_S) {
                     if constexpr (SPLIT_S_LO) {  // S(j) is in registers: columns 0-63 may take S(j+1)_lo
@@ -633,7 +652,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (last) {
                 const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
-                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (hh * g + rg % g) * D + hf * HD;
+                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (hq * g + rg % g) * D + hf * HD;
 #pragma unroll
                 for (int cb = 0; cb < HD / 32; ++cb) {
                     uint32_t v[32];
@@ -695,6 +714,7 @@ cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
     const int grid = (n_rows + 2 * BM - 1) / (2 * BM);
     const int heads = p.n_heads > 0 ? p.n_heads : 1;
     if (grid == 0) return cudaSuccess;
+    if (heads > MAX_LAUNCH_HEADS || p.q_span < 1 || p.kv_span < 1) return cudaErrorInvalidValue;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
@@ -703,17 +723,17 @@ cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
     if (attr_err != cudaSuccess) return attr_err;
     CUtensorMap tq, tk, tv;
     {
-        // (d, q heads of the launch's head group, tokens): head h's g rows start at coordinate h*g
-        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.g) * heads,
+        // (d, q heads spanned by the head map, tokens): kv head h's g rows start at coordinate h*g
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.g) * p.q_span,
                                     static_cast<cuuint64_t>(p.n_q)};
         const cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(p.q_tok_stride) * 2};
         const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(p.g), static_cast<cuuint32_t>(BM / p.g)};
         if (!make_tmap_bf16(&tq, p.q, 3, dims, strides, box)) return cudaErrorInvalidValue;
     }
     {
-        // (d, keys, kv heads of the group)
-        const int64_t hs = heads > 1 ? p.kv_head_stride : static_cast<int64_t>(p.n_k) * p.kv_row_stride;
-        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k), static_cast<cuuint64_t>(heads)};
+        // (d, keys, kv heads spanned by the head map)
+        const int64_t hs = p.kv_span > 1 ? p.kv_head_stride : static_cast<int64_t>(p.n_k) * p.kv_row_stride;
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k), static_cast<cuuint64_t>(p.kv_span)};
         const cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.kv_row_stride) * 2, static_cast<cuuint64_t>(hs) * 2};
         const cuuint32_t box[3] = {64, BN, 1};
         if (!make_tmap_bf16(&tk, p.k, 3, dims, strides, box)) return cudaErrorInvalidValue;

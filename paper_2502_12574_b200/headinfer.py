@@ -45,14 +45,27 @@ def _dev_tensor(t: torch.Tensor, shape, name: str) -> int:
 def hi_init(layers: int, q_heads: int, kv_heads: int, head_dim: int, max_ctx: int, chunk: int,
             rank: int = 0, world: int = 1, n_slots: int = 0, slot_tokens: int = 0, flags: int = 0,
             device: Optional[int] = None, numa_policy: int = 0, numa_node: int = 0,
-            resident_kv_heads: int = 0, head_group: int = 1) -> int:
-    """hi_init / hi_init_ex.  Returns the opaque context handle (an int)."""
+            resident_kv_heads: int = 0, head_group: int = 1, streaming_heads=None, duo_sink: int = 0,
+            duo_window: int = 0) -> int:
+    """hi_init / hi_init_ex.  Returns the opaque context handle (an int).
+
+    ``streaming_heads``: optional [layers, kv_heads] array-like of 0/1 (global kv heads), NEXT-3."""
     lib = _lib.load()
     handle = ctypes.c_void_p()
+    lab = None
+    if streaming_heads is not None:
+        lab = (ctypes.c_ubyte * (layers * kv_heads))()
+        flat = [int(x) for row in streaming_heads for x in row]
+        if len(flat) != layers * kv_heads:
+            raise ValueError(f"streaming_heads must be [layers={layers}, kv_heads={kv_heads}]")
+        for i, x in enumerate(flat):
+            lab[i] = 1 if x else 0
     opt = hi_options(n_slots=n_slots, slot_tokens=slot_tokens,
                      device=torch.cuda.current_device() if device is None else device,
                      flags=flags, numa_policy=numa_policy, numa_node=numa_node,
-                     resident_kv_heads=resident_kv_heads, head_group=head_group)
+                     resident_kv_heads=resident_kv_heads, head_group=head_group,
+                     streaming_heads=ctypes.cast(lab, ctypes.c_void_p) if lab is not None else None,
+                     duo_sink=duo_sink, duo_window=duo_window)
     st = lib.hi_init_ex(layers, q_heads, kv_heads, head_dim, max_ctx, chunk, rank, world,
                         ctypes.byref(opt), ctypes.byref(handle))
     if st != _lib.HI_OK:
