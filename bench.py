@@ -132,18 +132,24 @@ def gen_layer_inputs(layer, pos0, n, hq_loc, hkv_loc, d, q_head0, kv_head0, torc
     return Q, K, V
 
 
-def fill_history(hi, L, hkv_loc, kv_head0, d, upto, torch, fill_):
-    """Untimed: place the K/V of positions [0, upto) in the host store (same bytes a prefill writes)."""
+def fill_history(hi, L, hkv_loc, kv_head0, d, upto, torch, fill_, labels=None, duo=(0, 0)):
+    """Untimed: place the K/V of positions [0, upto) in the host store (same bytes a prefill writes).
+    Streaming heads (NEXT-3) keep only the sink rows and the last window rows: only those are written."""
     piece = 65536
     bk = torch.empty((piece, 1, d), dtype=torch.bfloat16, device="cuda")
     bv = torch.empty_like(bk)
     for l in range(L):
         for h in range(hkv_loc):
-            for p0 in range(0, upto, piece):
-                n = min(piece, upto - p0)
-                fill_(bk[:n], SEED, 1, DIST, l, kv_head0 + h, p0)
-                fill_(bv[:n], SEED, 2, DIST, l, kv_head0 + h, p0)
-                hi.write_host_kv(l, h, p0, bk[:n, 0], bv[:n, 0])
+            ranges = [(0, upto)]
+            if labels is not None and labels[l][kv_head0 + h]:
+                ns = min(max(duo[0], 0), upto)
+                ranges = [(0, ns), (max(ns, upto - duo[1]), upto)]
+            for lo, end in ranges:
+                for p0 in range(lo, end, piece):
+                    n = min(piece, end - p0)
+                    fill_(bk[:n], SEED, 1, DIST, l, kv_head0 + h, p0)
+                    fill_(bv[:n], SEED, 2, DIST, l, kv_head0 + h, p0)
+                    hi.write_host_kv(l, h, p0, bk[:n, 0], bv[:n, 0])
 
 
 def run_ours(args, rank, world, local_rank, pg):
@@ -180,12 +186,19 @@ def run_ours(args, rank, world, local_rank, pg):
         inputs_b = (K + 2) * L * c * (hq_loc + 2 * hkv_loc) * d * 2 + L * c * hq_loc * d * 2
         pair_b = 4 * d * max_ctx
         resident = int(max(0, min(L * hkv_loc, (free_b - inputs_b - (10 << 30)) // pair_b)))
+    labels, duo = None, (args.duo_sink, args.duo_window)
+    duo_opts = {}
+    if args.duo > 0:  # NEXT-3: synthetic duo-attention labels, `args.duo` of each layer's kv heads streaming
+        import synth
+        labels = synth.streaming_labels(SEED, L, hkv, args.duo)
+        duo_opts = dict(streaming_heads=labels.tolist(), duo_sink=args.duo_sink if args.duo_sink > 0 else -1,
+                        duo_window=args.duo_window)
     t0 = time.time()
     hi = HeadInfer(L, hq, hkv, d, max_ctx, c, rank, world, flags=HI_FLAG_TIMING, resident_kv_heads=resident,
-                   head_group=args.head_group)
+                   head_group=args.head_group, **duo_opts)
     init_s = time.time() - t0
     t0 = time.time()
-    fill_history(hi, L, hkv_loc, kv0h, d, s0, torch, fill_)
+    fill_history(hi, L, hkv_loc, kv0h, d, s0, torch, fill_, labels, duo)
     fill_s = time.time() - t0
     log(f"[rank {rank}] {wl}: init {init_s:.1f}s (host store {hi.stats()['host_store_bytes']/2**30:.1f} GiB), "
         f"history fill {fill_s:.1f}s")
@@ -332,10 +345,11 @@ def run_ours(args, rank, world, local_rank, pg):
     # step rooflines (measured peaks; sustained tensor peak inside a long step)
     pk = dict(peaks, bf16_tflops=peak_t)
     R = st1["resident_kv_heads"]
-    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, last_chunk_pos - c * (K - 1) // 2, c, world, R), pk)
-    t_roof_pre = sum(rf.step_roofline_seconds(rf.prefill_step(shape, s0 + (W + i) * c, c, world, R), pk)["seconds"]
+    dk = dict(streaming=st1["streaming_kv_heads"], n_sink=max(args.duo_sink, 0), win=args.duo_window)
+    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, last_chunk_pos - c * (K - 1) // 2, c, world, R, **dk), pk)
+    t_roof_pre = sum(rf.step_roofline_seconds(rf.prefill_step(shape, s0 + (W + i) * c, c, world, R, **dk), pk)["seconds"]
                      for i in range(K))
-    dec_roofs = [rf.step_roofline_seconds(rf.decode_step(shape, S + i, world, R), pk) for i in range(W, W + K)]
+    dec_roofs = [rf.step_roofline_seconds(rf.decode_step(shape, S + i, world, R, **dk), pk) for i in range(W, W + K)]
     t_roof_dec = sum(x["seconds"] for x in dec_roofs)
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "ncu_prefill_traffic.json")
@@ -362,6 +376,9 @@ def run_ours(args, rank, world, local_rank, pg):
                 "no weights: attention-only path)",
         "config": {"workload": wl, "layers": L, "q_heads": hq, "kv_heads": hkv, "head_dim": d, "context": S,
                    "chunk": c, "head_group": st1["head_group"], "resident_kv_heads": R,
+                   "duo": ({"streaming_frac": args.duo, "streaming_kv_heads": st1["streaming_kv_heads"],
+                            "sink": max(args.duo_sink, 0), "window": args.duo_window,
+                            "labels": "synthetic (synth.streaming_labels)"} if args.duo > 0 else None),
                    "parallelism": f"head-shard{world}", "prefill_step": "1 chunk x all layers",
                    "timed_chunk_positions": [s0 + W * c, last_chunk_pos],
                    "decode_step": "1 token x all layers", "decode_context": [S + W, S + W + K - 1],
@@ -394,10 +411,10 @@ def run_ours(args, rank, world, local_rank, pg):
         res["e2e"] = {"value": round(K * c / (e2e_ms / 1e3), 2), "unit": "tok/s",
                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
     if world > 1 and not args.no_cpu_baseline:
-        res["parity_sample"] = sharded_parity(gathered0, last_chunk_pos, L, hq, hkv, d, world, torch)
+        res["parity_sample"] = sharded_parity(gathered0, last_chunk_pos, L, hq, hkv, d, world, torch, labels, duo)
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"], res["parity_sample"] = cpu_baseline(hi, sample_out0, last_chunk_pos, dec_sample, dec_pos,
-                                                                 L, hq, hkv, d, torch)
+                                                                 L, hq, hkv, d, torch, labels=labels, duo=duo)
     hi.close()
     print(json.dumps(res), flush=True)
 
@@ -413,9 +430,18 @@ def _oracle_inputs_for_head(layer, kv_head, upto, d, torch):
     return k[:, 0], v[:, 0]
 
 
-def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d, torch, budget_s=15.0):
+def _oracle_rows(oracle, q, last, k, v, streaming, duo):
+    """The oracle for one head's rows: full causal (retrieval head) or sink + window (streaming head)."""
+    if streaming:
+        return oracle.attention_rows_duo(q, last, k, v, max(duo[0], 0), duo[1])
+    return oracle.attention_rows(q, last, k, v)
+
+
+def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d, torch, budget_s=15.0,
+                 labels=None, duo=(0, 0)):
     """Time the fp64 oracle (as it stands) on this box's host cores on a bounded sample of the same
-    workload: rows of layer 0's last timed prefill chunk; also check those rows against the GPU."""
+    workload: rows of layer 0's last timed prefill chunk; also check those rows against the GPU.
+    With duo labels (NEXT-3) the sampled streaming heads use the duo oracle."""
     import numpy as np
 
     import oracle
@@ -424,6 +450,11 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
     g = hq // hkv
     c = sample_out0.shape[0]
     heads = list(range(min(2, hkv)))   # kv heads sampled (q heads of their groups)
+    strm = {h: bool(labels is not None and labels[0][h]) for h in range(hkv)}
+    if labels is not None:             # one retrieval and one streaming head when both exist
+        r_h = [h for h in range(hkv) if not strm[h]][:1]
+        s_h = [h for h in range(hkv) if strm[h]][:1]
+        heads = (r_h + s_h) or heads
     kv = {h: _oracle_inputs_for_head(0, h, dec_pos + 1, d, torch) for h in heads}
     qpre = synth.gen_block(SEED, 0, DIST, 0, 0, hq, chunk_pos, c, d)
     # calibrate: one row per thread
@@ -438,7 +469,7 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
     k0, v0 = kv[heads[0]]
     probe_t = rows_for(cores)
     t0 = time.time()
-    oracle.attention_rows(qpre[probe_t, 0], chunk_pos + probe_t, k0, v0)
+    _oracle_rows(oracle, qpre[probe_t, heads[0] * g], chunk_pos + probe_t, k0, v0, strm[heads[0]], duo)
     rows_per_s = len(probe_t) / max(time.time() - t0, 1e-9)
     n_tok = int(max(2, min(c, budget_s * rows_per_s / (g * len(heads)))))
     toks = rows_for(n_tok)
@@ -448,7 +479,7 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
     for h in heads:
         k, v = kv[h]
         for j in range(h * g, (h + 1) * g):
-            ref = oracle.attention_rows(qpre[toks, j], chunk_pos + toks, k, v)
+            ref = _oracle_rows(oracle, qpre[toks, j], chunk_pos + toks, k, v, strm[h], duo)
             err = np.abs(got[toks, j] - ref)
             maxerr = max(maxerr, float(err.max()))
             sumerr += float(err.sum())
@@ -462,19 +493,19 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
     for h in heads:
         k, v = kv[h]
         for j in range(h * g, (h + 1) * g):
-            ref = oracle.attention_rows(qd[j:j + 1], np.array([dec_pos]), k, v)[0]
+            ref = _oracle_rows(oracle, qd[j:j + 1], np.array([dec_pos]), k, v, strm[h], duo)[0]
             dmax = max(dmax, float(np.abs(dgot[j] - ref).max()))
     rows_per_tok = L * hq
     cpu = {"value": round(rows / el / rows_per_tok, 6), "unit": "tok/s", "cores": cores, "kind": "oracle",
            "sample": f"{rows} (layer 0, q head, position) rows of the last timed prefill chunk at positions "
-                     f"{chunk_pos}+t, q heads 0..{len(heads) * g - 1}, {el:.1f}s; tok/s = rows/s / "
+                     f"{chunk_pos}+t, q heads of kv heads {heads}, {el:.1f}s; tok/s = rows/s / "
                      f"({L} layers x {hq} q heads)"}
     parity = {"prefill_rows": rows, "prefill_max_abs": maxerr, "prefill_mean_abs": sumerr / max(cnt, 1),
               "decode_rows": len(heads) * g, "decode_max_abs": dmax, "tol_max_abs": 2e-2, "tol_mean_abs": 2e-3}
     return cpu, parity
 
 
-def sharded_parity(gathered0, chunk_pos, L, hq, hkv, d, world, torch, n_tok=4):
+def sharded_parity(gathered0, chunk_pos, L, hq, hkv, d, world, torch, labels=None, duo=(0, 0), n_tok=4):
     """Head-sharded run: rows of the all-gathered layer-0 output of the last timed chunk, one q head
     per rank, against the oracle (checks the shard arithmetic + the collective end to end)."""
     import numpy as np
@@ -492,7 +523,7 @@ def sharded_parity(gathered0, chunk_pos, L, hq, hkv, d, world, torch, n_tok=4):
         j = r * (hq // world)          # first q head owned by rank r
         kv, v = _oracle_inputs_for_head(0, j // g, chunk_pos + c, d, torch)
         q = synth.gen_block(SEED, 0, DIST, 0, j, 1, chunk_pos, c, d)[toks, 0]
-        ref = oracle.attention_rows(q, chunk_pos + toks, kv, v)
+        ref = _oracle_rows(oracle, q, chunk_pos + toks, kv, v, bool(labels is not None and labels[0][j // g]), duo)
         maxerr = max(maxerr, float(np.abs(full[toks, j] - ref).max()))
     return {"gathered_rows": int(len(toks) * world), "max_abs": maxerr, "tol_max_abs": 2e-2}
 
@@ -564,6 +595,11 @@ def main():
                     help="NEXT-1: keep the first R (layer, kv head) pairs' KV in HBM (-1 = as many as fit)")
     ap.add_argument("--head-group", type=int, default=-1,
                     help="NEXT-2: kv heads per transfer/launch unit (-1 = auto: >= 8 waves per chunk launch)")
+    ap.add_argument("--duo", type=float, default=0.0,
+                    help="NEXT-3: fraction of each layer's kv heads that are duo-attention streaming heads "
+                         "(synthetic labels; the paper's extension table uses 0.5)")
+    ap.add_argument("--duo-sink", type=int, default=64, help="NEXT-3: attention-sink tokens of streaming heads")
+    ap.add_argument("--duo-window", type=int, default=256, help="NEXT-3: recent-window tokens of streaming heads")
     ap.add_argument("--ranks-share-gpu", action="store_true",
                     help="validation only: every rank uses cuda:0 and the output gather goes through gloo")
     args = ap.parse_args()

@@ -78,7 +78,7 @@ typedef struct hi_options {
      * with 1M KV cache" P:L988-1000): streaming_heads points at layers*kv_heads bytes (GLOBAL kv head index,
      * layer-major; the context reads its shard), nonzero = streaming head.  A streaming head is never
      * offloaded: its K/V live in HBM as duo_sink attention-sink rows plus a ring of the duo_window most
-     * recent rows ("keep the streaming head in the GPU", P:L966), and a query at position p attends exactly
+     * recent rows ("keep the streaming head in the GPU", P:L960), and a query at position p attends exactly
      * the keys i <= p with i < duo_sink or i > p - duo_window (reading R18).  The other (retrieval) heads
      * keep the full cache and are offloaded / resident / grouped as above.  The caller's array is copied.
      * NULL (default) = no streaming heads. */

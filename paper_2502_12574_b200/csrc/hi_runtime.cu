@@ -1015,12 +1015,15 @@ hi_status hi_read_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, v
                 return set_err(c, HI_ESTATE, "streaming head: row not held (only sink + recent window)");
         st = hi_synchronize(c);
         if (st != HI_OK) return st;
-        for (int64_t p = pos; p < pos + n; ++p) {
+        for (int64_t p = pos; p < pos + n;) {  // runs of positions that are contiguous rows (sink, ring segments)
             const int64_t r = c->duo_row(p);
+            const int64_t len = std::min(pos + n - p, p < c->duo_sink ? c->duo_sink - p : c->duo_rows - r);
+            const size_t b = static_cast<size_t>(len) * c->d * 2;
             uint8_t* kd = static_cast<uint8_t*>(k_dst) + (p - pos) * c->d * 2;
             uint8_t* vd = static_cast<uint8_t*>(v_dst) + (p - pos) * c->d * 2;
-            HI_CK(c, cudaMemcpy(kd, c->duo_k(layer, h, r), c->d * 2, cudaMemcpyDeviceToHost));
-            HI_CK(c, cudaMemcpy(vd, c->duo_k(layer, h, r) + c->duo_rows * c->d, c->d * 2, cudaMemcpyDeviceToHost));
+            HI_CK(c, cudaMemcpy(kd, c->duo_k(layer, h, r), b, cudaMemcpyDeviceToHost));
+            HI_CK(c, cudaMemcpy(vd, c->duo_k(layer, h, r) + c->duo_rows * c->d, b, cudaMemcpyDeviceToHost));
+            p += len;
         }
         return HI_OK;
     }
@@ -1049,13 +1052,16 @@ hi_status hi_write_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, 
     if (c->streaming(layer, h)) {  // NEXT-3: sink rows, then the last duo_ring rows of the range into the ring
         const cudaMemcpyKind kind = from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         const int64_t lo_ring = std::max<int64_t>(c->duo_sink, pos + n - c->duo_ring);
-        for (int64_t p = pos; p < pos + n; ++p) {
-            if (p >= c->duo_sink && p < lo_ring) continue;
+        for (int64_t p = pos; p < pos + n;) {  // runs of positions that are contiguous rows
+            if (p >= c->duo_sink && p < lo_ring) { p = lo_ring; continue; }
             const int64_t r = c->duo_row(p);
+            const int64_t len = std::min(pos + n - p, p < c->duo_sink ? c->duo_sink - p : c->duo_rows - r);
+            const size_t b = static_cast<size_t>(len) * c->d * 2;
             const uint8_t* ks = static_cast<const uint8_t*>(k_src) + (p - pos) * c->d * 2;
             const uint8_t* vs = static_cast<const uint8_t*>(v_src) + (p - pos) * c->d * 2;
-            HI_CK(c, cudaMemcpy(c->duo_k(layer, h, r), ks, c->d * 2, kind));
-            HI_CK(c, cudaMemcpy(c->duo_k(layer, h, r) + c->duo_rows * c->d, vs, c->d * 2, kind));
+            HI_CK(c, cudaMemcpy(c->duo_k(layer, h, r), ks, b, kind));
+            HI_CK(c, cudaMemcpy(c->duo_k(layer, h, r) + c->duo_rows * c->d, vs, b, kind));
+            p += len;
         }
         return HI_OK;
     }

@@ -50,30 +50,62 @@ def kv_bytes(d: int, tokens: int) -> int:
     return 4 * d * tokens
 
 
-def prefill_step(shape: Shape, s: int, n: int, world: int = 1, resident: int = 0) -> dict:
+def duo_keys(p: int, n_sink: int, win: int) -> int:
+    """Keys a duo-attention streaming head's query at position p attends (NEXT-3, reading R18):
+    |{i <= p : i < n_sink or i > p - win}| = min(p+1, n_sink) + max(0, p + 1 - max(n_sink, p - win + 1))."""
+    return min(p + 1, n_sink) + max(0, p + 1 - max(n_sink, p - win + 1))
+
+
+def duo_pairs(s: int, n: int, n_sink: int, win: int) -> int:
+    """Visible (query, key) pairs of a streaming head over chunk rows p in [s, s+n) (exact sum of duo_keys,
+    summed in closed form over the three regimes of p)."""
+    tot = 0
+    p, end = s, s + n
+    while p < end:
+        if p + 1 <= n_sink:                      # every key is a sink key: p + 1 keys
+            q = min(end, n_sink)
+            tot += (p + 1 + q) * (q - p) // 2    # sum_{x=p}^{q-1} (x+1)
+        elif p - win + 1 <= n_sink:              # window reaches into the sink: all p + 1 keys visible
+            q = min(end, n_sink + win)
+            tot += (p + 1 + q) * (q - p) // 2
+        else:                                    # sink + a full window
+            q = end
+            tot += (q - p) * (n_sink + win)
+        p = q
+    return tot
+
+
+def prefill_step(shape: Shape, s: int, n: int, world: int = 1, resident: int = 0, streaming: int = 0,
+                 n_sink: int = 64, win: int = 256) -> dict:
     """One prefill chunk over all layers on one rank (H_kv/world local heads); `resident` of the
-    rank's (layer, kv head) pairs keep their KV in HBM (NEXT-1): no link traffic, one HBM read."""
+    rank's retrieval (layer, kv head) pairs keep their KV in HBM (NEXT-1): no link traffic, one HBM read;
+    `streaming` pairs are duo streaming heads (NEXT-3): sink + window keys only, all in HBM."""
     pairs = shape.layers * (shape.kv_heads // world)
-    off = pairs - resident
+    retr = pairs - streaming
+    off = retr - resident
     d, g = shape.head_dim, shape.g
+    kept = min(s, n_sink + win)
     return {
-        "flops": pairs * prefill_flops(d, g, s, n),
+        "flops": retr * prefill_flops(d, g, s, n) + streaming * 4.0 * d * g * duo_pairs(s, n, n_sink, win),
         "h2d_bytes": off * kv_bytes(d, s),
         "d2h_bytes": off * kv_bytes(d, n),
-        "hbm_bytes": off * 2 * kv_bytes(d, s) + resident * kv_bytes(d, s)
+        "hbm_bytes": off * 2 * kv_bytes(d, s) + resident * kv_bytes(d, s) + streaming * kv_bytes(d, kept)
         + pairs * (kv_bytes(d, n) + 4 * d * g * n),
     }
 
 
-def decode_step(shape: Shape, s: int, world: int = 1, resident: int = 0) -> dict:
+def decode_step(shape: Shape, s: int, world: int = 1, resident: int = 0, streaming: int = 0,
+                n_sink: int = 64, win: int = 256) -> dict:
     pairs = shape.layers * (shape.kv_heads // world)
-    off = pairs - resident
+    retr = pairs - streaming
+    off = retr - resident
     d, g = shape.head_dim, shape.g
+    keys = duo_keys(s, n_sink, win)   # history keys + the new one
     return {
-        "flops": pairs * decode_flops(d, g, s),
+        "flops": retr * decode_flops(d, g, s) + streaming * 4.0 * d * g * keys,
         "h2d_bytes": off * kv_bytes(d, s),
         "d2h_bytes": off * kv_bytes(d, 1),
-        "hbm_bytes": off * 2 * kv_bytes(d, s) + resident * kv_bytes(d, s),
+        "hbm_bytes": off * 2 * kv_bytes(d, s) + resident * kv_bytes(d, s) + streaming * kv_bytes(d, keys),
     }
 
 

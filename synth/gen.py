@@ -115,7 +115,7 @@ def gen_qkv(seed: int, dist: str, layer: int, pos0: int, n_pos: int,
 
 def streaming_labels(seed: int, layers: int, kv_heads: int, frac: float = 0.5) -> np.ndarray:
     """Synthetic duo-attention head labels (NEXT-3; the paper's labels come from a trained model,
-    App. D P:L958): uint8 [layers, kv_heads], 1 = streaming head.  Exactly round(frac * kv_heads)
+    App. D P:L933): uint8 [layers, kv_heads], 1 = streaming head.  Exactly round(frac * kv_heads)
     streaming heads per layer, chosen by ranking a counter hash of (seed, layer, head) -- a pure
     function of its arguments, no method arithmetic."""
     n_str = int(round(frac * kv_heads))

@@ -86,3 +86,43 @@ def test_init_rejects_invalid_options(lib, opts):
     assert lib.hi_init_ex(1, 8, 4, 64, 1024, 256, 0, 1, ctypes.byref(o), ctypes.byref(h)) == 1
     assert not h.value
     assert b"hi_options" in lib.hi_last_error(None)
+
+
+@pytest.mark.parametrize("opts", [dict(duo_window=-5), dict(flags=0x10), dict(flags=0x20), dict(flags=0x40)])
+def test_init_rejects_invalid_duo_options(lib, opts):
+    """NEXT-3: streaming heads need a window >= 1 and the default (band-masking) prefill kernel."""
+    from paper_2502_12574_b200._lib import hi_options
+    lab = (ctypes.c_ubyte * 4)(1, 0, 0, 1)
+    h = ctypes.c_void_p()
+    o = hi_options(streaming_heads=ctypes.cast(lab, ctypes.c_void_p), **opts)
+    assert lib.hi_init_ex(1, 8, 4, 64, 1024, 256, 0, 1, ctypes.byref(o), ctypes.byref(h)) == 1
+    assert not h.value
+    assert b"streaming" in lib.hi_last_error(None)
+
+
+def test_init_rejects_too_many_local_kv_heads(lib):
+    h = ctypes.c_void_p()
+    assert lib.hi_init(1, 128, 128, 64, 1024, 256, 0, 1, ctypes.byref(h)) == 1  # > 64 kv heads per launch map
+    assert b"64" in lib.hi_last_error(None)
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The binding's hi_options / hi_stats mirror the C layout (size and every field offset), compiled
+    from include/headinfer.h with the host C compiler."""
+    import subprocess
+    from paper_2502_12574_b200._lib import hi_options, hi_stats
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "headinfer.h"', 'int main(void) {']
+    for st in (hi_options, hi_stats):
+        lines.append(f'printf("{st.__name__} %zu\\n", sizeof({st.__name__}));')
+        for name, _ in st._fields_:
+            lines.append(f'printf("{st.__name__}.{name} %zu\\n", offsetof({st.__name__}, {name}));')
+    lines += ["return 0; }"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines())
+    for st in (hi_options, hi_stats):
+        assert int(got[st.__name__]) == ctypes.sizeof(st), st.__name__
+        for name, _ in st._fields_:
+            assert int(got[f"{st.__name__}.{name}"]) == getattr(st, name).offset, (st.__name__, name)

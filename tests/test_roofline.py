@@ -68,3 +68,25 @@ def test_step_roofline_bound():
     assert dec["bound"] == "h2d"
     pre = rf.step_roofline_seconds(rf.prefill_step(S8B, 1 << 20, 16384), peaks)
     assert pre["bound"] == "tensor"
+
+
+def test_duo_counters_brute_force():
+    """NEXT-3 counters: duo_keys / duo_pairs against a direct enumeration of the visible key set
+    {i <= p : i < n_sink or i > p - win} (reading R18), across the sink / window regimes."""
+    for n_sink, win in [(0, 1), (3, 5), (64, 256), (10, 4), (7, 100)]:
+        for s in [0, 1, 5, 60, 300]:
+            for n in [1, 7, 130]:
+                brute = sum(1 for p in range(s, s + n) for i in range(p + 1) if i < n_sink or i > p - win)
+                assert rf.duo_pairs(s, n, n_sink, win) == brute, (n_sink, win, s, n)
+                assert rf.duo_keys(s + n - 1, n_sink, win) == sum(
+                    1 for i in range(s + n) if i < n_sink or i > s + n - 1 - win)
+
+
+def test_duo_step_reduces_to_plain_without_streaming():
+    a = rf.prefill_step(S8B, 4096, 1024, 1, 3)
+    b = rf.prefill_step(S8B, 4096, 1024, 1, 3, streaming=0)
+    assert a == b
+    # a window covering the context makes a streaming head cost what a resident head costs in FLOPs
+    c = rf.prefill_step(S8B, 4096, 1024, 1, 0, streaming=S8B.layers * S8B.kv_heads, n_sink=0, win=1 << 30)
+    assert c["flops"] == pytest.approx(a["flops"])
+    assert c["h2d_bytes"] == 0 and c["d2h_bytes"] == 0
