@@ -1,0 +1,75 @@
+/*
+ * hilayer.h -- C ABI of the synthetic Llama decoder layer around the head-wise offloaded attention
+ * path ("Full synthetic transformer layer around the path (QKV/O GEMMs, RoPE,
+ * MLP)", the paper's whole-model setting, §5, Tab. 6/7 P:L568-606).  Exported by the
+ * same libheadinfer.so as headinfer.h.
+ *
+ * One layer, in the paper's model family (Llama-3), inference only (weights are the caller's,
+ * random-init in benches and tests: no trained weights exist here).  For hidden states x [n, hidden]
+ * at global positions s .. s+n-1 (s = hi_seq_len(ctx, layer) before the call):
+ *
+ *   xn   = rmsnorm(x) * attn_norm                  (RMSNorm, eps rms_eps)
+ *   q|k|v = xn W_qkv^T                             (row-major weight [(Hq + 2 Hkv) d, hidden])
+ *   q, k = rope(q, k, position)                    (rotate-half RoPE, inv_freq_i = theta^(-2i/d))
+ *   a    = attention(q, k, v)                      (hi_prefill_chunk / hi_decode: the offloaded path)
+ *   x    = x + a W_o^T                             ([hidden, Hq d])
+ *   xn   = rmsnorm(x) * mlp_norm
+ *   g|u  = xn W_gate_up^T                          ([2 inter, hidden]: gate rows, then up rows)
+ *   x    = x + (silu(g) * u) W_down^T              ([hidden, inter])
+ *
+ * Storage is bf16 at every op boundary above (reading R19 in DESIGN.md); arithmetic inside an op is
+ * fp32 (GEMMs on cuBLASLt with fp32 accumulation, the norm / RoPE / SwiGLU in this library's kernels).
+ * Layout: every tensor is row-major, contiguous, bf16, on the context's device.  x is updated in place.
+ * Head sharding is not supported here (the context's world must be 1: a tensor-parallel layer needs an
+ * all-reduce after W_o and W_down that this round does not build).
+ *
+ * Ownership: the caller owns x and the weights; the model owns its workspaces (sized for the context's
+ * chunk) and never retains caller pointers.  All work is ordered on the caller's stream.
+ * Errors: hi_status codes as in headinfer.h; a CUDA or cuBLAS failure returns HI_ECUDA.
+ */
+#ifndef HILAYER_H_
+#define HILAYER_H_
+
+#include "headinfer.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hl_model hl_model; /* opaque; one per hi_ctx */
+
+/* One decoder layer's weights: device pointers, bf16, row-major [out, in] (PyTorch Linear layout). */
+typedef struct hl_weights {
+    const void* attn_norm;  /* [hidden] */
+    const void* w_qkv;      /* [(Hq + 2 Hkv) * head_dim, hidden]: q heads, then k heads, then v heads */
+    const void* w_o;        /* [hidden, Hq * head_dim] */
+    const void* mlp_norm;   /* [hidden] */
+    const void* w_gate_up;  /* [2 * inter, hidden]: gate rows [0, inter), up rows [inter, 2 inter) */
+    const void* w_down;     /* [hidden, inter] */
+} hl_weights;
+
+/*
+ * hl_create -- workspaces (for up to the context's `chunk` tokens) and a cuBLASLt handle for layers
+ * around `ctx`'s attention.  hidden, inter: multiples of 64; rope_theta > 0; rms_eps > 0.
+ * Errors: HI_EINVAL (sizes, world != 1), HI_ENOMEM_DEV, HI_ECUDA.
+ */
+hi_status hl_create(hi_ctx* ctx, int hidden, int inter, double rope_theta, float rms_eps, hl_model** out);
+
+/* One prefill chunk of one layer: x [n, hidden] in place (n in [1, chunk]); the attention step is
+ * hi_prefill_chunk on the same layer (so seq_len[layer] advances by n).  Errors as hi_prefill_chunk. */
+hi_status hl_prefill_chunk(hl_model* m, int layer, const hl_weights* w, void* x, int n, void* cuda_stream);
+
+/* One decode token of one layer: x [hidden] in place; the attention step is hi_decode. */
+hi_status hl_decode(hl_model* m, int layer, const hl_weights* w, void* x, void* cuda_stream);
+
+/* Release the workspaces (the hi_ctx is not freed).  NULL is a no-op. */
+hi_status hl_free(hl_model* m);
+
+/* Message describing the model's last failure (or of the last failed hl_create when m is NULL). */
+const char* hl_last_error(const hl_model* m);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HILAYER_H_ */

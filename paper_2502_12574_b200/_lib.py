@@ -26,10 +26,11 @@ HI_FLAG_PREFILL_TC1 = 0x40
 HI_RESIDENT_AUTO = -1
 HI_GROUP_AUTO = -1
 
-# every symbol include/headinfer.h declares (checked by tests/test_abi.py)
+# every symbol include/headinfer.h and include/hilayer.h declare (checked by tests/test_abi.py)
 EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",
            "hi_write_host_kv", "hi_seq_len", "hi_set_seq_len", "hi_get_stats", "hi_synchronize",
-           "hi_status_str", "hi_last_error"]
+           "hi_status_str", "hi_last_error",
+           "hl_create", "hl_prefill_chunk", "hl_decode", "hl_free", "hl_last_error"]
 
 
 class hi_options(ctypes.Structure):
@@ -37,6 +38,12 @@ class hi_options(ctypes.Structure):
                 ("flags", ctypes.c_int), ("numa_policy", ctypes.c_int), ("numa_node", ctypes.c_int),
                 ("resident_kv_heads", ctypes.c_int), ("head_group", ctypes.c_int),
                 ("streaming_heads", ctypes.c_void_p), ("duo_sink", ctypes.c_int), ("duo_window", ctypes.c_int)]
+
+
+class hl_weights(ctypes.Structure):
+    """include/hilayer.h: one decoder layer's weights (device pointers, bf16, row-major [out, in])."""
+    _fields_ = [("attn_norm", ctypes.c_void_p), ("w_qkv", ctypes.c_void_p), ("w_o", ctypes.c_void_p),
+                ("mlp_norm", ctypes.c_void_p), ("w_gate_up", ctypes.c_void_p), ("w_down", ctypes.c_void_p)]
 
 
 class hi_stats(ctypes.Structure):
@@ -87,6 +94,14 @@ def load() -> ctypes.CDLL:
     lib.hi_status_str.restype = ctypes.c_char_p
     lib.hi_last_error.argtypes = [P]
     lib.hi_last_error.restype = ctypes.c_char_p
+    lib.hl_create.argtypes = [P, I, I, ctypes.c_double, ctypes.c_float, ctypes.POINTER(P)]
+    lib.hl_prefill_chunk.argtypes = [P, I, ctypes.POINTER(hl_weights), VP, I, VP]
+    lib.hl_decode.argtypes = [P, I, ctypes.POINTER(hl_weights), VP, VP]
+    lib.hl_free.argtypes = [P]
+    lib.hl_last_error.argtypes = [P]
+    lib.hl_last_error.restype = ctypes.c_char_p
+    for name in ["hl_create", "hl_prefill_chunk", "hl_decode", "hl_free"]:
+        getattr(lib, name).restype = I
     if hasattr(lib, "hi_debug_prefill_trace"):  # HI_TRACE variant builds only
         lib.hi_debug_prefill_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
         lib.hi_debug_prefill_trace.restype = ctypes.c_int

@@ -5,7 +5,8 @@
 Outputs
   paper_2502_12574_b200/libheadinfer.so   -- the C ABI (include/headinfer.h) + kernels
   synth/libsynth.so                       -- seeded input generator twin (test/bench infra)
-cudart is linked statically (nvcc default), so the libraries load on a GPU-less host too.
+cudart is linked statically (nvcc default), so the libraries load on a GPU-less host too; cuBLASLt
+(NEXT-4 layer GEMMs) is linked dynamically from /usr/local/cuda/lib64 (rpath).
 """
 from __future__ import annotations
 
@@ -28,7 +29,10 @@ def _stale(out: str, srcs) -> bool:
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def _nvcc_shared(out: str, srcs, extra=(), force=False, verbose=False):
+CUDA_LIB = "/usr/local/cuda/lib64"
+
+
+def _nvcc_shared(out: str, srcs, extra=(), force=False, verbose=False, libs=()):
     deps = list(srcs) + glob.glob(os.path.join(os.path.dirname(srcs[0]), "*.cuh")) + \
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     if not force and not _stale(out, deps):
@@ -55,9 +59,13 @@ def _nvcc_shared(out: str, srcs, extra=(), force=False, verbose=False):
     if failed:
         raise RuntimeError("nvcc compilation failed")
     tmp = out + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread", *libs])
     os.replace(tmp, out)
     return out
+
+
+# cuBLASLt for the NEXT-4 layer's plain GEMMs (hl_layer.cu), found at run time through the rpath
+HI_LIBS = ["-L" + CUDA_LIB, "-lcublasLt", "-Xlinker", "-rpath=" + CUDA_LIB]
 
 
 def build_variant(name: str, defines) -> str:
@@ -66,12 +74,12 @@ def build_variant(name: str, defines) -> str:
     srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
     out = os.path.join(PKG, "build", "variants", f"libheadinfer_{name}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    return _nvcc_shared(out, srcs, extra=[f"-D{d}" for d in defines], force=True)
+    return _nvcc_shared(out, srcs, extra=[f"-D{d}" for d in defines], force=True, libs=HI_LIBS)
 
 
 def build(force: bool = False, verbose: bool = False) -> None:
     srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
-    _nvcc_shared(os.path.join(PKG, "libheadinfer.so"), srcs, force=force, verbose=verbose)
+    _nvcc_shared(os.path.join(PKG, "libheadinfer.so"), srcs, force=force, verbose=verbose, libs=HI_LIBS)
     ssrc = sorted(glob.glob(os.path.join(ROOT, "synth", "csrc", "*.cu")))
     _nvcc_shared(os.path.join(ROOT, "synth", "libsynth.so"), ssrc, force=force, verbose=verbose)
 

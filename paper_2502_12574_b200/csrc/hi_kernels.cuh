@@ -6,7 +6,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+struct hi_ctx;  // include/headinfer.h
+
 namespace hi {
+
+// Context geometry for the layer wrapper (hl_layer.cu, NEXT-4); false on NULL.
+struct CtxInfo {
+    int L, Hq_loc, Hkv_loc, d, chunk, world, device;
+};
+bool ctx_info(const hi_ctx* c, CtxInfo* out);
 
 // TMA tensor map over a bf16 tensor, SWIZZLE_128B, (tmap.cu); dims/strides innermost-first, strides in
 // bytes (rank-1 entries).  false if the driver entry point is unavailable or the encode fails.

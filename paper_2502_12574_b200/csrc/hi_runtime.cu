@@ -413,6 +413,12 @@ hi_status finish_call(hi_ctx* c, cudaStream_t cs) {
 
 }  // namespace
 
+bool hi::ctx_info(const hi_ctx* c, hi::CtxInfo* o) {
+    if (!c || !o) return false;
+    *o = {c->L, c->Hq_loc, c->Hkv_loc, c->d, c->chunk, c->world, c->device};
+    return true;
+}
+
 extern "C" {
 
 const char* hi_status_str(hi_status s) {

@@ -1,0 +1,337 @@
+// hl_layer.cu -- NEXT-4: the synthetic Llama decoder layer around the head-wise offloaded attention path
+// (include/hilayer.h; the paper's whole-model setting).
+//
+// Per call, on the caller's stream:
+//   rmsnorm_kernel      xn = bf16(x * rsqrt(mean(x^2) + eps) * gamma)          (fp32 inside)
+//   cuBLASLt GEMM       qkv = bf16(xn W_qkv^T)                                 (fp32 accumulate)
+//   rope_split_kernel   Q, K = bf16(rope(q, k)), V = v, split head-major for the attention call
+//   hi_prefill_chunk / hi_decode   a = attention(Q, K, V)                      (the offloaded path)
+//   cuBLASLt GEMM       x = bf16(x + a W_o^T)          (beta = 1, D aliases C: the residual is the epilogue)
+//   rmsnorm_kernel      xn = ... mlp_norm
+//   cuBLASLt GEMM       gu = bf16(xn W_gate_up^T)
+//   swiglu_kernel       act = bf16(silu(g) * u)
+//   cuBLASLt GEMM       x = bf16(x + act W_down^T)
+// The GEMMs are plain library GEMMs (cuBLASLt); the elementwise / normalisation steps are HBM-bound
+// one-pass kernels with 16-byte accesses.  RoPE angles are reduced in fp64 (p * inv_freq reaches 1e6 rad
+// at 1M context, where an fp32 product would already be off by ~0.06 rad), then sin/cos in fp32.
+#include "../../include/hilayer.h"
+#include "hi_kernels.cuh"
+
+#include <cublasLt.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <tuple>
+
+namespace {
+
+thread_local std::string g_hl_error = "no error";
+constexpr int MAX_HALF_D = 64;  // head_dim <= 128
+
+struct RopeParams {
+    const __nv_bfloat16* qkv;  // [n][(hq + 2 hkv) * d]
+    __nv_bfloat16* q;          // [n][hq][d]
+    __nv_bfloat16* k;          // [n][hkv][d]
+    __nv_bfloat16* v;          // [n][hkv][d]
+    int n, hq, hkv, d;
+    int64_t pos0;
+    double inv_freq[MAX_HALF_D];
+};
+
+__device__ __forceinline__ float bf(const __nv_bfloat16 x) { return __bfloat162float(x); }
+
+// One CTA per row: sum of squares in fp32 (8 bf16 per 16-byte load), then one rounding per output.
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      const __nv_bfloat16* __restrict__ gamma,
+                                                      __nv_bfloat16* __restrict__ out, int h, float eps) {
+    const int64_t row = blockIdx.x;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
+    const uint4* gr = reinterpret_cast<const uint4*>(gamma);
+    uint4* orow = reinterpret_cast<uint4*>(out + row * h);
+    const int n8 = h / 8;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < n8; i += blockDim.x) {
+        const uint4 u = xr[i];
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ss += bf(e[j]) * bf(e[j]);
+    }
+    __shared__ float red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+    for (int w = 0; w < (blockDim.x >> 5); ++w) tot += red[w];
+    const float rinv = rsqrtf(tot / static_cast<float>(h) + eps);
+    for (int i = threadIdx.x; i < n8; i += blockDim.x) {
+        const uint4 u = xr[i], gu = gr[i];
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&u);
+        const __nv_bfloat16* g = reinterpret_cast<const __nv_bfloat16*>(&gu);
+        uint4 w;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&w);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(bf(e[j]) * rinv * bf(g[j]));
+        orow[i] = w;
+    }
+}
+
+// One CTA per token: cos/sin of the token's d/2 angles once (fp64 range reduction), then every q and k
+// head's pairs (i, i + d/2) rotated (rotate-half convention) and V copied, into head-major tensors.
+__global__ void __launch_bounds__(256) rope_split_kernel(const RopeParams p) {
+    __shared__ float cs[MAX_HALF_D], sn[MAX_HALF_D];
+    const int t = blockIdx.x;
+    const int half = p.d / 2;
+    if (threadIdx.x < half) {
+        const double two_pi = 6.283185307179586476925286766559;
+        double a = static_cast<double>(p.pos0 + t) * p.inv_freq[threadIdx.x];
+        a -= two_pi * floor(a / two_pi);
+        float s, c;
+        sincosf(static_cast<float>(a), &s, &c);
+        cs[threadIdx.x] = c;
+        sn[threadIdx.x] = s;
+    }
+    __syncthreads();
+    const int row = (p.hq + 2 * p.hkv) * p.d;
+    const __nv_bfloat16* in = p.qkv + static_cast<int64_t>(t) * row;
+    const int rot_pairs = (p.hq + p.hkv) * half;
+    for (int i = threadIdx.x; i < rot_pairs; i += blockDim.x) {
+        const int hd = i / half, j = i % half;  // heads [0, hq) are q, [hq, hq + hkv) are k
+        const float x1 = bf(in[hd * p.d + j]), x2 = bf(in[hd * p.d + j + half]);
+        const float o1 = x1 * cs[j] - x2 * sn[j];
+        const float o2 = x2 * cs[j] + x1 * sn[j];
+        __nv_bfloat16* dst = hd < p.hq ? p.q + (static_cast<int64_t>(t) * p.hq + hd) * p.d
+                                       : p.k + (static_cast<int64_t>(t) * p.hkv + (hd - p.hq)) * p.d;
+        dst[j] = __float2bfloat16_rn(o1);
+        dst[j + half] = __float2bfloat16_rn(o2);
+    }
+    const int v8 = p.hkv * p.d / 8;
+    const uint4* vin = reinterpret_cast<const uint4*>(in + (p.hq + p.hkv) * p.d);
+    uint4* vout = reinterpret_cast<uint4*>(p.v + static_cast<int64_t>(t) * p.hkv * p.d);
+    for (int i = threadIdx.x; i < v8; i += blockDim.x) vout[i] = vin[i];
+}
+
+// act[t][c] = bf16(silu(g) * u), g = gu[t][c], u = gu[t][inter + c]; 8 columns per thread.
+__global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act, int n,
+                              int inter) {
+    const int c8 = inter / 8;
+    const int64_t total = static_cast<int64_t>(n) * c8;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t t = i / c8;
+        const int c = static_cast<int>(i % c8);
+        const uint4 gv = reinterpret_cast<const uint4*>(gu + t * 2 * inter)[c];
+        const uint4 uv = reinterpret_cast<const uint4*>(gu + t * 2 * inter + inter)[c];
+        const __nv_bfloat16* g = reinterpret_cast<const __nv_bfloat16*>(&gv);
+        const __nv_bfloat16* u = reinterpret_cast<const __nv_bfloat16*>(&uv);
+        uint4 w;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&w);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float x = bf(g[j]);
+            o[j] = __float2bfloat16_rn(x / (1.f + expf(-x)) * bf(u[j]));
+        }
+        reinterpret_cast<uint4*>(act + t * inter)[c] = w;
+    }
+}
+
+}  // namespace
+
+struct hl_model {
+    hi_ctx* ctx = nullptr;
+    hi::CtxInfo ci{};
+    int H = 0, I = 0;
+    float eps = 0.f;
+    double inv_freq[MAX_HALF_D] = {0};
+    std::string err = "no error";
+    cublasLtHandle_t lt = nullptr;
+    void* lt_ws = nullptr;
+    size_t lt_ws_bytes = size_t(32) << 20;
+    std::map<std::tuple<int, int, int, int>, cublasLtMatmulAlgo_t> algos;
+    __nv_bfloat16 *xn = nullptr, *qkv = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr,
+                  *gu = nullptr, *act = nullptr;
+    int64_t launches = 0;
+};
+
+namespace {
+
+hi_status hl_fail(hl_model* m, hi_status s, const std::string& msg) {
+    if (m) m->err = msg;
+    else g_hl_error = msg;
+    return s;
+}
+
+hi_status ck(hl_model* m, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return HI_OK;
+    cudaGetLastError();
+    return hl_fail(m, HI_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Y[n, mo] (+)= X[n, k] W[mo, k]^T, all row-major bf16; beta 0 or 1 (1: Y holds the residual, D aliases C).
+hi_status gemm(hl_model* m, const __nv_bfloat16* W, const __nv_bfloat16* X, __nv_bfloat16* Y, int mo, int n, int kd,
+               float beta, cudaStream_t st) {
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+    cublasStatus_t s = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F);
+    const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
+    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof tA);
+    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof tB);
+    // column-major view: A = W^T stored [kd x mo] (ld kd), op T -> mo x kd; B = X^T [kd x n]; C = Y^T [mo x n]
+    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatrixLayoutCreate(&la, CUDA_R_16BF, kd, mo, kd);
+    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatrixLayoutCreate(&lb, CUDA_R_16BF, kd, n, kd);
+    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatrixLayoutCreate(&lc, CUDA_R_16BF, mo, n, mo);
+    const auto key = std::make_tuple(mo, n, kd, beta != 0.f ? 1 : 0);
+    auto it = m->algos.find(key);
+    if (s == CUBLAS_STATUS_SUCCESS && it == m->algos.end()) {
+        cublasLtMatmulPreference_t pref = nullptr;
+        s = cublasLtMatmulPreferenceCreate(&pref);
+        if (s == CUBLAS_STATUS_SUCCESS)
+            s = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &m->lt_ws_bytes,
+                                                     sizeof m->lt_ws_bytes);
+        cublasLtMatmulHeuristicResult_t res{};
+        int found = 0;
+        if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatmulAlgoGetHeuristic(m->lt, op, la, lb, lc, lc, pref, 1, &res, &found);
+        if (pref) cublasLtMatmulPreferenceDestroy(pref);
+        if (s == CUBLAS_STATUS_SUCCESS && found == 0) s = CUBLAS_STATUS_NOT_SUPPORTED;
+        if (s == CUBLAS_STATUS_SUCCESS) it = m->algos.emplace(key, res.algo).first;
+    }
+    const float alpha = 1.f;
+    if (s == CUBLAS_STATUS_SUCCESS)
+        s = cublasLtMatmul(m->lt, op, &alpha, W, la, X, lb, &beta, Y, lc, Y, lc, &it->second, m->lt_ws, m->lt_ws_bytes, st);
+    if (lc) cublasLtMatrixLayoutDestroy(lc);
+    if (lb) cublasLtMatrixLayoutDestroy(lb);
+    if (la) cublasLtMatrixLayoutDestroy(la);
+    if (op) cublasLtMatmulDescDestroy(op);
+    if (s != CUBLAS_STATUS_SUCCESS) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "cuBLASLt matmul %dx%dx%d failed (status %d)", mo, n, kd, static_cast<int>(s));
+        return hl_fail(m, HI_ECUDA, buf);
+    }
+    return HI_OK;
+}
+
+hi_status rmsnorm(hl_model* m, const __nv_bfloat16* x, const void* gamma, __nv_bfloat16* out, int n, cudaStream_t st) {
+    rmsnorm_kernel<<<n, 256, 0, st>>>(x, static_cast<const __nv_bfloat16*>(gamma), out, m->H, m->eps);
+    ++m->launches;
+    return ck(m, cudaGetLastError(), "rmsnorm_kernel");
+}
+
+// Everything of the layer except the attention call; `attend` runs hi_prefill_chunk / hi_decode.
+template <typename Attend>
+hi_status layer(hl_model* m, int layer_idx, const hl_weights* w, void* xv, int n, cudaStream_t st, Attend attend) {
+    if (!m) return HI_ESHAPE;
+    if (!w || !xv || !w->attn_norm || !w->w_qkv || !w->w_o || !w->mlp_norm || !w->w_gate_up || !w->w_down)
+        return hl_fail(m, HI_ESHAPE, "NULL weight or activation pointer");
+    if (layer_idx < 0 || layer_idx >= m->ci.L) return hl_fail(m, HI_ESHAPE, "layer out of range");
+    const int64_t s = hi_seq_len(m->ctx, layer_idx);
+    __nv_bfloat16* x = static_cast<__nv_bfloat16*>(xv);
+    const int hq = m->ci.Hq_loc, hkv = m->ci.Hkv_loc, d = m->ci.d;
+    hi_status r;
+    if ((r = rmsnorm(m, x, w->attn_norm, m->xn, n, st)) != HI_OK) return r;
+    if ((r = gemm(m, static_cast<const __nv_bfloat16*>(w->w_qkv), m->xn, m->qkv, (hq + 2 * hkv) * d, n, m->H, 0.f, st)) != HI_OK)
+        return r;
+    RopeParams rp{};
+    rp.qkv = m->qkv;
+    rp.q = m->q;
+    rp.k = m->k;
+    rp.v = m->v;
+    rp.n = n;
+    rp.hq = hq;
+    rp.hkv = hkv;
+    rp.d = d;
+    rp.pos0 = s;
+    for (int i = 0; i < d / 2; ++i) rp.inv_freq[i] = m->inv_freq[i];
+    rope_split_kernel<<<n, 256, 0, st>>>(rp);
+    ++m->launches;
+    if ((r = ck(m, cudaGetLastError(), "rope_split_kernel")) != HI_OK) return r;
+    if ((r = attend()) != HI_OK) {
+        m->err = std::string("attention: ") + hi_last_error(m->ctx);
+        return r;
+    }
+    if ((r = gemm(m, static_cast<const __nv_bfloat16*>(w->w_o), m->attn, x, m->H, n, hq * d, 1.f, st)) != HI_OK) return r;
+    if ((r = rmsnorm(m, x, w->mlp_norm, m->xn, n, st)) != HI_OK) return r;
+    if ((r = gemm(m, static_cast<const __nv_bfloat16*>(w->w_gate_up), m->xn, m->gu, 2 * m->I, n, m->H, 0.f, st)) != HI_OK)
+        return r;
+    const int64_t work = static_cast<int64_t>(n) * (m->I / 8);
+    const int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 8));
+    swiglu_kernel<<<grid, 256, 0, st>>>(m->gu, m->act, n, m->I);
+    ++m->launches;
+    if ((r = ck(m, cudaGetLastError(), "swiglu_kernel")) != HI_OK) return r;
+    return gemm(m, static_cast<const __nv_bfloat16*>(w->w_down), m->act, x, m->H, n, m->I, 1.f, st);
+}
+
+void destroy(hl_model* m) {
+    if (!m) return;
+    cudaDeviceSynchronize();
+    for (__nv_bfloat16* p : {m->xn, m->qkv, m->q, m->k, m->v, m->attn, m->gu, m->act}) cudaFree(p);
+    cudaFree(m->lt_ws);
+    if (m->lt) cublasLtDestroy(m->lt);
+    cudaGetLastError();
+    delete m;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hl_last_error(const hl_model* m) { return m ? m->err.c_str() : g_hl_error.c_str(); }
+
+hi_status hl_create(hi_ctx* ctx, int hidden, int inter, double rope_theta, float rms_eps, hl_model** out) {
+    if (!out) return hl_fail(nullptr, HI_EINVAL, "out is NULL");
+    *out = nullptr;
+    hi::CtxInfo ci{};
+    if (!hi::ctx_info(ctx, &ci)) return hl_fail(nullptr, HI_EINVAL, "ctx is NULL");
+    if (hidden <= 0 || inter <= 0 || hidden % 64 || inter % 64 || !(rope_theta > 0.0) || !(rms_eps > 0.f))
+        return hl_fail(nullptr, HI_EINVAL, "hidden and inter must be positive multiples of 64; rope_theta, rms_eps > 0");
+    if (ci.world != 1) return hl_fail(nullptr, HI_EINVAL, "the layer wrapper needs world == 1 (no tensor parallelism)");
+    hl_model* m = new hl_model();
+    m->ctx = ctx;
+    m->ci = ci;
+    m->H = hidden;
+    m->I = inter;
+    m->eps = rms_eps;
+    for (int i = 0; i < ci.d / 2; ++i) m->inv_freq[i] = pow(rope_theta, -2.0 * i / ci.d);
+    auto bail = [&](hi_status s, const char* msg) {
+        cudaGetLastError();
+        destroy(m);
+        return hl_fail(nullptr, s, msg);
+    };
+    if (cudaSetDevice(ci.device) != cudaSuccess) return bail(HI_ECUDA, "cudaSetDevice failed");
+    const size_t c = static_cast<size_t>(ci.chunk);
+    const size_t elems[8] = {c * hidden, c * (ci.Hq_loc + 2 * ci.Hkv_loc) * ci.d, c * ci.Hq_loc * ci.d,
+                             c * ci.Hkv_loc * ci.d, c * ci.Hkv_loc * ci.d, c * ci.Hq_loc * ci.d,
+                             c * 2 * inter, c * inter};
+    __nv_bfloat16** bufs[8] = {&m->xn, &m->qkv, &m->q, &m->k, &m->v, &m->attn, &m->gu, &m->act};
+    for (int i = 0; i < 8; ++i)
+        if (cudaMalloc(reinterpret_cast<void**>(bufs[i]), elems[i] * 2) != cudaSuccess)
+            return bail(HI_ENOMEM_DEV, "cudaMalloc of a layer workspace failed");
+    if (cudaMalloc(&m->lt_ws, m->lt_ws_bytes) != cudaSuccess) return bail(HI_ENOMEM_DEV, "cuBLASLt workspace");
+    if (cublasLtCreate(&m->lt) != CUBLAS_STATUS_SUCCESS) return bail(HI_ECUDA, "cublasLtCreate failed");
+    *out = m;
+    return HI_OK;
+}
+
+hi_status hl_prefill_chunk(hl_model* m, int layer_idx, const hl_weights* w, void* x, int n, void* cuda_stream) {
+    if (m && (n < 1 || n > m->ci.chunk)) return hl_fail(m, HI_ESHAPE, "n_tokens must be in [1, chunk]");
+    return layer(m, layer_idx, w, x, n, static_cast<cudaStream_t>(cuda_stream), [&] {
+        return hi_prefill_chunk(m->ctx, layer_idx, m->q, m->k, m->v, m->attn, n, cuda_stream);
+    });
+}
+
+hi_status hl_decode(hl_model* m, int layer_idx, const hl_weights* w, void* x, void* cuda_stream) {
+    return layer(m, layer_idx, w, x, 1, static_cast<cudaStream_t>(cuda_stream), [&] {
+        return hi_decode(m->ctx, layer_idx, m->q, m->k, m->v, m->attn, cuda_stream);
+    });
+}
+
+hi_status hl_free(hl_model* m) {
+    destroy(m);
+    return HI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+"""Thin Python binding of the NEXT-4 layer ABI (include/hilayer.h) -- argument marshalling only.
+
+``HeadInferLayer`` wraps an ``hl_model`` around a ``HeadInfer`` context: every step of the layer
+(RMSNorm, GEMMs, RoPE, SwiGLU, the offloaded attention) runs in libheadinfer.so on the caller's stream.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import HIError, hl_weights
+from .headinfer import HeadInfer, _dev_tensor, _stream_ptr
+
+WEIGHT_NAMES = ("attn_norm", "w_qkv", "w_o", "mlp_norm", "w_gate_up", "w_down")
+
+
+class HeadInferLayer:
+    """Synthetic Llama decoder layers (weights supplied per call) around one HeadInfer context."""
+
+    def __init__(self, hi: HeadInfer, hidden: int, inter: int, rope_theta: float = 500000.0, rms_eps: float = 1e-5):
+        self.hi, self.hidden, self.inter = hi, hidden, inter
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        st = lib.hl_create(hi.handle, hidden, inter, rope_theta, rms_eps, ctypes.byref(h))
+        if st != _lib.HI_OK:
+            raise HIError(st, lib.hl_last_error(None).decode(errors="replace"))
+        self._m = h.value
+        self._wcache = {}
+
+    def _weights(self, w: dict) -> hl_weights:
+        hq, hkv, d, H, I = self.hi.hq_loc, self.hi.hkv_loc, self.hi.head_dim, self.hidden, self.inter
+        shapes = {"attn_norm": (H,), "w_qkv": ((hq + 2 * hkv) * d, H), "w_o": (H, hq * d), "mlp_norm": (H,),
+                  "w_gate_up": (2 * I, H), "w_down": (H, I)}
+        return hl_weights(**{k: _dev_tensor(w[k], shapes[k], k) for k in WEIGHT_NAMES})
+
+    def _check(self, st: int) -> None:
+        if st != _lib.HI_OK:
+            raise HIError(st, _lib.load().hl_last_error(self._m).decode(errors="replace"))
+
+    def prefill_chunk(self, layer: int, w: dict, x: torch.Tensor, stream: Optional[torch.cuda.Stream] = None):
+        """x [n, hidden] bf16, updated in place to the layer's output."""
+        n = x.shape[0]
+        ptr = _dev_tensor(x, (n, self.hidden), "x")
+        ws = self._weights(w)
+        self._check(_lib.load().hl_prefill_chunk(self._m, layer, ctypes.byref(ws), ptr, n, _stream_ptr(stream)))
+        return x
+
+    def decode(self, layer: int, w: dict, x: torch.Tensor, stream: Optional[torch.cuda.Stream] = None):
+        """x [hidden] bf16 (one token), updated in place."""
+        ptr = _dev_tensor(x, (self.hidden,), "x")
+        ws = self._weights(w)
+        self._check(_lib.load().hl_decode(self._m, layer, ctypes.byref(ws), ptr, _stream_ptr(stream)))
+        return x
+
+    def close(self) -> None:
+        if getattr(self, "_m", None):
+            _lib.load().hl_free(self._m)
+            self._m = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

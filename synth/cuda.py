@@ -47,3 +47,31 @@ def gen_block_cuda(seed: int, tensor: int, dist: str, layer: int, head0: int, n_
                    d: int, device=None) -> torch.Tensor:
     out = torch.empty((n_pos, n_heads, d), dtype=torch.bfloat16, device=device or "cuda")
     return fill_(out, seed, tensor, dist, layer, head0, pos0)
+
+
+def fill_matrix_(out: torch.Tensor, seed: int, tensor: int, layer: int, scale_log2: int = 0, row0: int = 0) -> torch.Tensor:
+    """GPU twin of synth.gen_matrix: fill a contiguous CUDA bf16 [rows, cols] (or [cols]) tensor."""
+    flat = out.view(-1, out.shape[-1]) if out.dim() == 2 else out.view(1, -1)
+    rows, cols = flat.shape
+    if cols % 128:
+        raise ValueError("cols must be a multiple of 128")
+    fill_(flat.view(rows, cols // 128, 128), seed, tensor, "U", layer, 0, row0)
+    if scale_log2:
+        out.mul_(2.0 ** scale_log2)  # a power of two: exact in bf16
+    return out
+
+
+def gen_layer_weights_cuda(seed: int, layer: int, hidden: int, inter: int, q_heads: int, kv_heads: int, d: int) -> dict:
+    """GPU twin of synth.gen_layer_weights (same bits)."""
+    from .gen import (TENSOR_ATTN_NORM, TENSOR_MLP_NORM, TENSOR_WDOWN, TENSOR_WGU, TENSOR_WO, TENSOR_WQKV,
+                      layer_weight_scales)
+    sc = layer_weight_scales(hidden, inter, q_heads * d)
+    e = lambda *shape: torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+    return {
+        "attn_norm": fill_matrix_(e(hidden), seed, TENSOR_ATTN_NORM, layer),
+        "w_qkv": fill_matrix_(e((q_heads + 2 * kv_heads) * d, hidden), seed, TENSOR_WQKV, layer, sc["w_qkv"]),
+        "w_o": fill_matrix_(e(hidden, q_heads * d), seed, TENSOR_WO, layer, sc["w_o"]),
+        "mlp_norm": fill_matrix_(e(hidden), seed, TENSOR_MLP_NORM, layer),
+        "w_gate_up": fill_matrix_(e(2 * inter, hidden), seed, TENSOR_WGU, layer, sc["w_gate_up"]),
+        "w_down": fill_matrix_(e(hidden, inter), seed, TENSOR_WDOWN, layer, sc["w_down"]),
+    }

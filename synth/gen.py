@@ -31,6 +31,8 @@ from __future__ import annotations
 import numpy as np
 
 TENSOR_Q, TENSOR_K, TENSOR_V = 0, 1, 2
+# NEXT-4 synthetic decoder layer: hidden-state input and the layer's random-init weights
+TENSOR_X, TENSOR_ATTN_NORM, TENSOR_WQKV, TENSOR_WO, TENSOR_MLP_NORM, TENSOR_WGU, TENSOR_WDOWN = 3, 4, 5, 6, 7, 8, 9
 DISTS = ("U", "P", "S", "ONE")
 DIST_ID = {name: i for i, name in enumerate(DISTS)}
 BASE_SEED = 0x48454144  # "HEAD"
@@ -81,7 +83,7 @@ def gen_block(seed: int, tensor: int, dist: str, layer: int, head0: int, n_heads
     """
     if dist not in DIST_ID:
         raise ValueError(f"unknown dist {dist!r}")
-    if not (0 <= tensor < 4 and 0 <= layer < 128 and 0 <= head0 and head0 + n_heads <= 128
+    if not (0 <= tensor < 16 and 0 <= layer < 128 and 0 <= head0 and head0 + n_heads <= 128
             and 0 <= pos0 and pos0 + n_pos <= (1 << 23) and 0 < d <= 256):
         raise ValueError("coordinate out of generator range")
     if dist == "ONE" and tensor == TENSOR_V:
@@ -111,6 +113,38 @@ def gen_qkv(seed: int, dist: str, layer: int, pos0: int, n_pos: int,
     k = gen_block(seed, TENSOR_K, dist, layer, kv_head0, kv_heads, pos0, n_pos, d)
     v = gen_block(seed, TENSOR_V, dist, layer, kv_head0, kv_heads, pos0, n_pos, d)
     return q, k, v
+
+
+def gen_matrix(seed: int, tensor: int, layer: int, rows: int, cols: int, scale_log2: int = 0,
+               row0: int = 0) -> np.ndarray:
+    """bf16 bits [rows, cols] for the NEXT-4 layer tensors (distribution U): element (r, c) is the generator
+    value at (tensor, layer, head = c // 128, pos = row0 + r, dim = c % 128), times 2^scale_log2 (a power of
+    two: exact in bf16).  cols must be a multiple of 128 (at most 128 * 128)."""
+    if cols % 128 or cols // 128 > 128:
+        raise ValueError("cols must be a multiple of 128, at most 16384")
+    b = gen_block(seed, tensor, "U", layer, 0, cols // 128, row0, rows, 128).reshape(rows, cols)
+    if scale_log2:
+        b = f32_to_bf16_rne(bf16_to_f32(b) * np.float32(2.0 ** scale_log2))
+    return b
+
+
+def layer_weight_scales(hidden: int, inter: int, q_dim: int) -> dict:
+    """Power-of-two weight scales keeping the synthetic layer's activations O(1): 2^(1 - floor(log2(fan_in)/2))."""
+    sc = lambda fan_in: 1 - (int(np.log2(fan_in)) // 2)
+    return {"w_qkv": sc(hidden), "w_o": sc(q_dim), "w_gate_up": sc(hidden), "w_down": sc(inter)}
+
+
+def gen_layer_weights(seed: int, layer: int, hidden: int, inter: int, q_heads: int, kv_heads: int, d: int) -> dict:
+    """Random-init bf16 weights of one synthetic Llama decoder layer (include/hilayer.h layouts)."""
+    sc = layer_weight_scales(hidden, inter, q_heads * d)
+    return {
+        "attn_norm": gen_matrix(seed, TENSOR_ATTN_NORM, layer, 1, hidden)[0],
+        "w_qkv": gen_matrix(seed, TENSOR_WQKV, layer, (q_heads + 2 * kv_heads) * d, hidden, sc["w_qkv"]),
+        "w_o": gen_matrix(seed, TENSOR_WO, layer, hidden, q_heads * d, sc["w_o"]),
+        "mlp_norm": gen_matrix(seed, TENSOR_MLP_NORM, layer, 1, hidden)[0],
+        "w_gate_up": gen_matrix(seed, TENSOR_WGU, layer, 2 * inter, hidden, sc["w_gate_up"]),
+        "w_down": gen_matrix(seed, TENSOR_WDOWN, layer, hidden, inter, sc["w_down"]),
+    }
 
 
 def streaming_labels(seed: int, layers: int, kv_heads: int, frac: float = 0.5) -> np.ndarray:

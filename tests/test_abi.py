@@ -12,9 +12,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _declared_symbols():
-    src = open(os.path.join(ROOT, "include", "headinfer.h")).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(hi_[a-z_]+)\s*\(", src)))
+    syms = set()
+    for hdr in ("headinfer.h", "hilayer.h"):
+        src = open(os.path.join(ROOT, "include", hdr)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        syms |= set(re.findall(r"\b(h[il]_[a-z_]+)\s*\(", src))
+    return sorted(syms)
 
 
 @pytest.fixture(scope="module")
@@ -110,9 +113,10 @@ def test_ctypes_structs_match_the_header(tmp_path):
     """The binding's hi_options / hi_stats mirror the C layout (size and every field offset), compiled
     from include/headinfer.h with the host C compiler."""
     import subprocess
-    from paper_2502_12574_b200._lib import hi_options, hi_stats
+    from paper_2502_12574_b200._lib import hi_options, hi_stats, hl_weights
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "headinfer.h"', 'int main(void) {']
-    for st in (hi_options, hi_stats):
+    lines[2] = '#include "hilayer.h"'
+    for st in (hi_options, hi_stats, hl_weights):
         lines.append(f'printf("{st.__name__} %zu\\n", sizeof({st.__name__}));')
         for name, _ in st._fields_:
             lines.append(f'printf("{st.__name__}.{name} %zu\\n", offsetof({st.__name__}, {name}));')
@@ -122,7 +126,7 @@ def test_ctypes_structs_match_the_header(tmp_path):
     exe = tmp_path / "layout"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines())
-    for st in (hi_options, hi_stats):
+    for st in (hi_options, hi_stats, hl_weights):
         assert int(got[st.__name__]) == ctypes.sizeof(st), st.__name__
         for name, _ in st._fields_:
             assert int(got[f"{st.__name__}.{name}"]) == getattr(st, name).offset, (st.__name__, name)
