@@ -41,6 +41,10 @@ WORKLOADS = {
 }
 SEED = 0x48454144
 DIST = "U"  # throughput workload
+# --model (NEXT-4): Llama-3-8B decoder-layer dims around the attention path (hidden, intermediate)
+MODEL_DIMS = (4096, 14336)
+MODEL_ROPE_THETA = 500000.0
+MODEL_RMS_EPS = 1e-5
 
 
 def log(*a):
@@ -184,6 +188,9 @@ def run_ours(args, rank, world, local_rank, pg):
     if resident < 0:  # as many (layer, kv head) pairs as fit next to this bench's inputs (NEXT-1)
         free_b, _ = torch.cuda.mem_get_info()
         inputs_b = (K + 2) * L * c * (hq_loc + 2 * hkv_loc) * d * 2 + L * c * hq_loc * d * 2
+        if args.model:  # 32 layers of weights + the layer workspaces
+            H, I = MODEL_DIMS
+            inputs_b += L * (H * (hq + 2 * hkv) * d + H * hq * d + 3 * H * I) * 2 + c * (4 * H + 3 * I) * 2
         pair_b = 4 * d * max_ctx
         resident = int(max(0, min(L * hkv_loc, (free_b - inputs_b - (10 << 30)) // pair_b)))
     labels, duo = None, (args.duo_sink, args.duo_window)
@@ -214,8 +221,31 @@ def run_ours(args, rank, world, local_rank, pg):
 
     gathered0 = None
 
+    # ---------------- the step: attention path only (default), or whole synthetic layers (--model, NEXT-4)
+    model = None
+    if args.model:
+        from paper_2502_12574_b200.layer import HeadInferLayer
+        from synth.cuda import fill_matrix_, gen_layer_weights_cuda
+        if world != 1:
+            raise SystemExit("--model runs at world 1 (the layer wrapper has no tensor parallelism)")
+        H, I = MODEL_DIMS
+        model = HeadInferLayer(hi, H, I, MODEL_ROPE_THETA, MODEL_RMS_EPS)
+        weights = [gen_layer_weights_cuda(SEED, l, H, I, hq, hkv, d) for l in range(L)]
+        torch.cuda.synchronize()
+
+    def make_inputs(pos, n):
+        """One step's inputs: per-layer (Q, K, V) for the attention path; x [n, H] for --model."""
+        if model is not None:
+            return fill_matrix_(torch.empty((n, MODEL_DIMS[0]), dtype=torch.bfloat16, device="cuda"), SEED,
+                                synth_tensor_x, 0, row0=pos)
+        return [gen_layer_inputs(l, pos, n, hq_loc, hkv_loc, d, q0h, kv0h, torch, fill_) for l in range(L)]
+
     def prefill_step(inputs, outs):
         nonlocal gathered, gathered0
+        if model is not None:   # x flows through every layer in place; outs[0] keeps layer 0's input copy
+            for l in range(L):
+                model.prefill_chunk(l, weights[l], inputs)
+            return
         for l in range(L):
             Q, Kt, Vt = inputs[l]
             hi.prefill_chunk(l, Q, Kt, Vt, outs[l])
@@ -225,14 +255,15 @@ def run_ours(args, rank, world, local_rank, pg):
                 else:
                     gathered = gather_heads(outs[l], group=pg, out=gathered)
 
+    synth_tensor_x = 3  # synth.TENSOR_X
+
     # ---------------- prefill: W warm-up chunks, then K timed chunks (all inputs resident) -------
     outs = [torch.empty((c, hq_loc, d), dtype=torch.bfloat16, device="cuda") for _ in range(L)]
     for i in range(W):
-        inputs = [gen_layer_inputs(l, s0 + i * c, c, hq_loc, hkv_loc, d, q0h, kv0h, torch, fill_) for l in range(L)]
+        inputs = make_inputs(s0 + i * c, c)
         prefill_step(inputs, outs)
         del inputs
-    timed_inputs = [[gen_layer_inputs(l, s0 + (W + i) * c, c, hq_loc, hkv_loc, d, q0h, kv0h, torch, fill_)
-                     for l in range(L)] for i in range(K)]
+    timed_inputs = [make_inputs(s0 + (W + i) * c, c) for i in range(K)]
     hi.synchronize()
     st0 = hi.stats()
     torch.cuda.synchronize()
@@ -253,13 +284,16 @@ def run_ours(args, rank, world, local_rank, pg):
     del timed_inputs
 
     # ---------------- decode: W warm-up tokens, then K timed tokens at context S ----------------
-    dq = [[gen_layer_inputs(l, S + i, 1, hq_loc, hkv_loc, d, q0h, kv0h, torch, fill_) for l in range(L)]
-          for i in range(W + K)]
+    dq = [make_inputs(S + i, 1) for i in range(W + K)]
     dout = [torch.empty((hq_loc, d), dtype=torch.bfloat16, device="cuda") for _ in range(L)]
     gdec = None
 
     def decode_step(i):
         nonlocal gdec
+        if model is not None:
+            for l in range(L):
+                model.decode(l, weights[l], dq[i][0])
+            return
         for l in range(L):
             q, k, v = dq[i][l]
             hi.decode(l, q[0], k[0], v[0], dout[l])
@@ -290,28 +324,41 @@ def run_ours(args, rank, world, local_rank, pg):
     if not args.no_e2e:
         for l in range(L):
             hi.set_seq_len(l, s0 + W * c)
-        host_in = [[torch.empty(t_shape, dtype=torch.bfloat16).pin_memory() for t_shape in
-                    ((c, hq_loc, d), (c, hkv_loc, d), (c, hkv_loc, d))] for _ in range(L)]
-        host_out = [torch.empty((c, hq_loc, d), dtype=torch.bfloat16).pin_memory() for _ in range(L)]
-        dev_in = [[torch.empty(t.shape, dtype=t.dtype, device="cuda") for t in host_in[l]] for l in range(L)]
+        if model is not None:   # x in, x out (the last layer's hidden states)
+            shapes = [[(c, MODEL_DIMS[0])]]
+            out_shape = (c, MODEL_DIMS[0])
+        else:
+            shapes = [[(c, hq_loc, d), (c, hkv_loc, d), (c, hkv_loc, d)] for _ in range(L)]
+            out_shape = (c, hq_loc, d)
+        host_in = [[torch.empty(sh, dtype=torch.bfloat16).pin_memory() for sh in per] for per in shapes]
+        host_out = [torch.empty(out_shape, dtype=torch.bfloat16).pin_memory() for _ in shapes]
+        dev_in = [[torch.empty(t.shape, dtype=t.dtype, device="cuda") for t in per] for per in host_in]
         e2e_ms = 0.0
-        h2d_b = sum(t.numel() * 2 for l in range(L) for t in host_in[l])
+        h2d_b = sum(t.numel() * 2 for per in host_in for t in per)
         d2h_b = sum(t.numel() * 2 for t in host_out)
         for i in range(K):
-            for l in range(L):   # untimed: this step's inputs into pinned host buffers
-                for t_dev, t_host in zip(gen_layer_inputs(l, s0 + (W + i) * c, c, hq_loc, hkv_loc, d, q0h, kv0h,
-                                                          torch, fill_), host_in[l]):
+            step_in = make_inputs(s0 + (W + i) * c, c)   # untimed: this step's inputs into pinned host buffers
+            step_in = [[step_in]] if model is not None else step_in
+            for per_dev, per_host in zip(step_in, host_in):
+                for t_dev, t_host in zip(per_dev, per_host):
                     t_host.copy_(t_dev)
+            del step_in
             torch.cuda.synchronize()
             barrier()
             e0.record(stream)
-            for l in range(L):
-                for t_dev, t_host in zip(dev_in[l], host_in[l]):
-                    t_dev.copy_(t_host, non_blocking=True)
-                hi.prefill_chunk(l, *dev_in[l], outs[l])
-                if world > 1:
-                    gathered = gather_heads(outs[l], group=pg, out=gathered)
-                host_out[l].copy_(outs[l], non_blocking=True)
+            if model is not None:
+                dev_in[0][0].copy_(host_in[0][0], non_blocking=True)
+                for l in range(L):
+                    model.prefill_chunk(l, weights[l], dev_in[0][0])
+                host_out[0].copy_(dev_in[0][0], non_blocking=True)
+            else:
+                for l in range(L):
+                    for t_dev, t_host in zip(dev_in[l], host_in[l]):
+                        t_dev.copy_(t_host, non_blocking=True)
+                    hi.prefill_chunk(l, *dev_in[l], outs[l])
+                    if world > 1:
+                        gathered = gather_heads(outs[l], group=pg, out=gathered)
+                    host_out[l].copy_(outs[l], non_blocking=True)
             hi.synchronize()
             e1.record(stream)
             torch.cuda.synchronize()
@@ -412,7 +459,23 @@ def run_ours(args, rank, world, local_rank, pg):
                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
     if world > 1 and not args.no_cpu_baseline:
         res["parity_sample"] = sharded_parity(gathered0, last_chunk_pos, L, hq, hkv, d, world, torch, labels, duo)
-    if world == 1 and not args.no_cpu_baseline:
+    if model is not None:
+        H, I = MODEL_DIMS
+        gemm_tok = L * 2.0 * (H * (hq + 2 * hkv) * d + H * hq * d + 3 * H * I)  # QKV, O, gate+up, down
+        t_gemm = K * c * gemm_tok / (peak_t * 1e12)
+        res["config"]["path"] = "synthetic Llama-3-8B decoder layers (NEXT-4): RMSNorm, QKV/O/MLP GEMMs, RoPE, SwiGLU"
+        res["data"] = ("synthetic (seeded counter-hash generator): hidden states in, random-init Llama-3-8B layer "
+                       "weights (no trained weights, no embedding / LM head)")
+        res["config"]["hidden"], res["config"]["intermediate"] = H, I
+        res["model"] = {"prefill_tok_s": round(tok_s, 2), "decode_ms_per_token": round(dec_ms_tok, 3),
+                        "gemm_flops_per_token": gemm_tok,
+                        "attention_share_of_prefill": round(pf_ms / pre_ms, 4) if pre_ms else None,
+                        "step_roofline_frac": round((t_roof_pre + t_gemm) / (pre_ms / 1e3), 4),
+                        "parity": "tests/test_gpu_layer.py (layer oracle, incl. one 8B-shaped layer)",
+                        "note": "history K/V below the timed chunks are synthetic (placed untimed), not produced "
+                                "by running the layers; no embedding / LM head"}
+        model.close()
+    if world == 1 and not args.no_cpu_baseline and model is None:
         res["cpu_baseline"], res["parity_sample"] = cpu_baseline(hi, sample_out0, last_chunk_pos, dec_sample, dec_pos,
                                                                  L, hq, hkv, d, torch, labels=labels, duo=duo)
     hi.close()
@@ -595,6 +658,9 @@ def main():
                     help="NEXT-1: keep the first R (layer, kv head) pairs' KV in HBM (-1 = as many as fit)")
     ap.add_argument("--head-group", type=int, default=-1,
                     help="NEXT-2: kv heads per transfer/launch unit (-1 = auto: >= 8 waves per chunk launch)")
+    ap.add_argument("--model", action="store_true",
+                    help="NEXT-4: time whole synthetic Llama-3-8B decoder layers (RMSNorm, QKV/O/MLP GEMMs, RoPE, "
+                         "SwiGLU) around the attention path instead of the attention path alone")
     ap.add_argument("--duo", type=float, default=0.0,
                     help="NEXT-3: fraction of each layer's kv heads that are duo-attention streaming heads "
                          "(synthetic labels; the paper's extension table uses 0.5)")
