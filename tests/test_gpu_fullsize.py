@@ -1,5 +1,6 @@
 """Full-size parity: the Llama-3-8B head geometry at the 128K context of BASELINE.json configs[1],
-in bench.py's launch configuration (chunk 18944, 4 staging slots of max_ctx/4 tokens), on sampled
+in bench.py's launch configuration (chunk 18944, 4 staging slots of max_ctx/4 tokens, head groups as
+bench.py picks them; also with 50% duo streaming heads, NEXT-3), on sampled
 rows the oracle computes one by one, plus a bit-exact host-KV scan.  Layers are reduced to 2 (every
 layer call runs the identical launch sequence)."""
 import numpy as np
@@ -19,13 +20,24 @@ def _gen(tensor, dist, layer, head0, nh, pos0, n, d):
     return gen_block_cuda(SEED, tensor, dist, layer, head0, nh, pos0, n, d)
 
 
-@pytest.mark.parametrize("dist", ["U", "P"])
-def test_llama8b_128k_sampled_rows_and_host_kv(dist):
-    from oracle import attention_rows
+@pytest.mark.parametrize("dist,opts", [
+    ("U", {}),
+    ("P", {}),
+    ("P", {"head_group": -1}),                                                 # bench.py's default unit size
+    ("S", {"head_group": -1, "duo": 0.5}),                                     # NEXT-3 at full size
+])
+def test_llama8b_128k_sampled_rows_and_host_kv(dist, opts):
+    from oracle import attention_rows, attention_rows_duo
     from paper_2502_12574_b200.headinfer import HeadInfer
     L, hq, hkv, d, S, c, n_dec = 2, 32, 8, 128, 131072, 18944, 3
     g = hq // hkv
-    hi = HeadInfer(L, hq, hkv, d, S + n_dec, c)
+    opts = dict(opts)
+    labels = None
+    n_sink, win = 64, 256
+    if opts.pop("duo", 0):
+        labels = synth.streaming_labels(SEED, L, hkv, 0.5)
+        opts.update(streaming_heads=labels.tolist(), duo_sink=n_sink, duo_window=win)
+    hi = HeadInfer(L, hq, hkv, d, S + n_dec, c, **opts)
     sample = {}  # (layer) -> list of (pos, out row [hq, d])
     rng = np.random.default_rng(0)
     chunk_starts = list(range(0, S, c))
@@ -58,12 +70,18 @@ def test_llama8b_128k_sampled_rows_and_host_kv(dist):
         for h in range(hkv):
             k = _gen(1, dist, layer, h, 1, 0, S + n_dec, d)[:, 0].cpu().view(torch.int16).numpy().view(np.uint16)
             v = _gen(2, dist, layer, h, 1, 0, S + n_dec, d)[:, 0].cpu().view(torch.int16).numpy().view(np.uint16)
-            # host KV store must hold exactly these bytes
-            hk, hv = hi.read_host_kv(layer, h, 0, S + n_dec)
-            assert np.array_equal(hk.view(torch.int16).numpy().view(np.uint16), k), (layer, h)
-            assert np.array_equal(hv.view(torch.int16).numpy().view(np.uint16), v), (layer, h)
+            streaming = labels is not None and labels[layer][h]
+            # host KV store must hold exactly these bytes (a streaming head: its sink and its window)
+            spans = [(0, n_sink), (S + n_dec - win, S + n_dec)] if streaming else [(0, S + n_dec)]
+            for lo, hi_ in spans:
+                hk, hv = hi.read_host_kv(layer, h, lo, hi_ - lo)
+                assert np.array_equal(hk.view(torch.int16).numpy().view(np.uint16), k[lo:hi_]), (layer, h)
+                assert np.array_equal(hv.view(torch.int16).numpy().view(np.uint16), v[lo:hi_]), (layer, h)
             for j in range(h * g, (h + 1) * g):
-                ref = attention_rows(qpos[:, j], pos, k, v)
+                if streaming:
+                    ref = attention_rows_duo(qpos[:, j], pos, k, v, n_sink, win)
+                else:
+                    ref = attention_rows(qpos[:, j], pos, k, v)
                 err = np.abs(got[:, j] - ref)
                 maxerr = max(maxerr, float(err.max()))
                 sumerr += float(err.sum())
