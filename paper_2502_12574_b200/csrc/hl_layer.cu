@@ -99,16 +99,18 @@ __global__ void __launch_bounds__(256) rope_split_kernel(const RopeParams p) {
     __syncthreads();
     const int row = (p.hq + 2 * p.hkv) * p.d;
     const __nv_bfloat16* in = p.qkv + static_cast<int64_t>(t) * row;
-    const int rot_pairs = (p.hq + p.hkv) * half;
-    for (int i = threadIdx.x; i < rot_pairs; i += blockDim.x) {
-        const int hd = i / half, j = i % half;  // heads [0, hq) are q, [hq, hq + hkv) are k
-        const float x1 = bf(in[hd * p.d + j]), x2 = bf(in[hd * p.d + j + half]);
-        const float o1 = x1 * cs[j] - x2 * sn[j];
-        const float o2 = x2 * cs[j] + x1 * sn[j];
+    const int h2 = half / 2;  // each thread rotates two adjacent pairs: 4-byte loads / stores
+    const int rot = (p.hq + p.hkv) * h2;
+    for (int i = threadIdx.x; i < rot; i += blockDim.x) {
+        const int hd = i / h2, j = 2 * (i % h2);  // heads [0, hq) are q, [hq, hq + hkv) are k
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(in + hd * p.d + j));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(in + hd * p.d + j + half));
         __nv_bfloat16* dst = hd < p.hq ? p.q + (static_cast<int64_t>(t) * p.hq + hd) * p.d
                                        : p.k + (static_cast<int64_t>(t) * p.hkv + (hd - p.hq)) * p.d;
-        dst[j] = __float2bfloat16_rn(o1);
-        dst[j + half] = __float2bfloat16_rn(o2);
+        *reinterpret_cast<__nv_bfloat162*>(dst + j) =
+            __floats2bfloat162_rn(a.x * cs[j] - b.x * sn[j], a.y * cs[j + 1] - b.y * sn[j + 1]);
+        *reinterpret_cast<__nv_bfloat162*>(dst + j + half) =
+            __floats2bfloat162_rn(b.x * cs[j] + a.x * sn[j], b.y * cs[j + 1] + a.y * sn[j + 1]);
     }
     const int v8 = p.hkv * p.d / 8;
     const uint4* vin = reinterpret_cast<const uint4*>(in + (p.hq + p.hkv) * p.d);
