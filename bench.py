@@ -38,6 +38,10 @@ WORKLOADS = {
     "8B-1M": (32, 32, 8, 128, 1 << 20, 18944),
     "8B-128K": (32, 32, 8, 128, 131072, 18944),
     "tiny": (1, 4, 2, 64, 1024, 128),
+    # configs[3] / configs[4] are 8-GPU head-sharded workloads; on one GPU they run as one rank's share
+    # (--emulate-shard 0/8): 1 kv head per layer.  70B: g = 8, so 9472 tokens x 8 rows = 2 full waves.
+    "8B-4M": (32, 32, 8, 128, 4 << 20, 18944),
+    "70B-1M": (80, 64, 8, 128, 1 << 20, 9472),
 }
 SEED = 0x48454144
 DIST = "U"  # throughput workload
@@ -174,7 +178,13 @@ def run_ours(args, rank, world, local_rank, pg):
         dist.broadcast(t, 0)
         wl = list(WORKLOADS)[int(t.item())]
     L, hq, hkv, d, S, c = WORKLOADS[wl]
-    sh = shard(hq, hkv, rank, world)
+    # head shard: this process's rank, or (--emulate-shard R/W) rank R of a W-GPU job run alone on this GPU
+    hr, hw = (rank, world) if args.emulate_shard is None else args.emulate_shard
+    sh = shard(hq, hkv, hr, hw)
+    host_need = L * (hkv // hw) * 4 * d * (S + 2 * (K + W) + 8) * (world if args.emulate_shard is None else 1)
+    if mem_available_bytes() < host_need + (24 << 30):   # a box driven out of memory is a strike
+        raise SystemExit(f"workload {wl}: host store {host_need / 2**30:.0f} GiB does not fit in MemAvailable "
+                         f"{mem_available_bytes() / 2**30:.0f} GiB with a 24 GiB margin")
     hq_loc, hkv_loc, q0h, kv0h = sh["q_local"], sh["kv_local"], sh["q"][0], sh["kv"][0]
     n_pre = W + K
     s0 = S - K * c - W * c                   # first warm-up chunk position
@@ -201,7 +211,7 @@ def run_ours(args, rank, world, local_rank, pg):
         duo_opts = dict(streaming_heads=labels.tolist(), duo_sink=args.duo_sink if args.duo_sink > 0 else -1,
                         duo_window=args.duo_window)
     t0 = time.time()
-    hi = HeadInfer(L, hq, hkv, d, max_ctx, c, rank, world, flags=HI_FLAG_TIMING, resident_kv_heads=resident,
+    hi = HeadInfer(L, hq, hkv, d, max_ctx, c, hr, hw, flags=HI_FLAG_TIMING, resident_kv_heads=resident,
                    head_group=args.head_group, **duo_opts)
     init_s = time.time() - t0
     t0 = time.time()
@@ -393,10 +403,10 @@ def run_ours(args, rank, world, local_rank, pg):
     pk = dict(peaks, bf16_tflops=peak_t)
     R = st1["resident_kv_heads"]
     dk = dict(streaming=st1["streaming_kv_heads"], n_sink=max(args.duo_sink, 0), win=args.duo_window)
-    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, last_chunk_pos - c * (K - 1) // 2, c, world, R, **dk), pk)
-    t_roof_pre = sum(rf.step_roofline_seconds(rf.prefill_step(shape, s0 + (W + i) * c, c, world, R, **dk), pk)["seconds"]
+    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, last_chunk_pos - c * (K - 1) // 2, c, hw, R, **dk), pk)
+    t_roof_pre = sum(rf.step_roofline_seconds(rf.prefill_step(shape, s0 + (W + i) * c, c, hw, R, **dk), pk)["seconds"]
                      for i in range(K))
-    dec_roofs = [rf.step_roofline_seconds(rf.decode_step(shape, S + i, world, R, **dk), pk) for i in range(W, W + K)]
+    dec_roofs = [rf.step_roofline_seconds(rf.decode_step(shape, S + i, hw, R, **dk), pk) for i in range(W, W + K)]
     t_roof_dec = sum(x["seconds"] for x in dec_roofs)
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "ncu_prefill_traffic.json")
@@ -426,7 +436,9 @@ def run_ours(args, rank, world, local_rank, pg):
                    "duo": ({"streaming_frac": args.duo, "streaming_kv_heads": st1["streaming_kv_heads"],
                             "sink": max(args.duo_sink, 0), "window": args.duo_window,
                             "labels": "synthetic (synth.streaming_labels)"} if args.duo > 0 else None),
-                   "parallelism": f"head-shard{world}", "prefill_step": "1 chunk x all layers",
+                   "parallelism": (f"head-shard{world}" if args.emulate_shard is None else
+                                   f"rank {hr} of head-shard{hw}, run alone on 1 GPU (no all-gather)"),
+                   "prefill_step": "1 chunk x all layers",
                    "timed_chunk_positions": [s0 + W * c, last_chunk_pos],
                    "decode_step": "1 token x all layers", "decode_context": [S + W, S + W + K - 1],
                    "l2": "inputs per step > L2 (>= 6 GiB), no flush needed"},
@@ -477,7 +489,15 @@ def run_ours(args, rank, world, local_rank, pg):
         model.close()
     if world == 1 and not args.no_cpu_baseline and model is None:
         res["cpu_baseline"], res["parity_sample"] = cpu_baseline(hi, sample_out0, last_chunk_pos, dec_sample, dec_pos,
-                                                                 L, hq, hkv, d, torch, labels=labels, duo=duo)
+                                                                 L, hq, hkv, d, torch, labels=labels, duo=duo,
+                                                                 kv0=kv0h, hkv_loc=hkv_loc)
+    if args.emulate_shard is not None:
+        res["shard_emulation"] = {
+            "rank": hr, "world": hw, "kv_heads": list(sh["kv"]), "q_heads": list(sh["q"]),
+            "note": "one rank's share of a head-sharded job, measured alone on one GPU: every rank does the same "
+                    "work on its own heads (no K/V crosses GPUs), so value is the job's tok/s if the W ranks run "
+                    "as fast as this one; the per-layer output all-gather and any host-link sharing between "
+                    "ranks are not measured"}
     hi.close()
     print(json.dumps(res), flush=True)
 
@@ -501,7 +521,7 @@ def _oracle_rows(oracle, q, last, k, v, streaming, duo):
 
 
 def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d, torch, budget_s=15.0,
-                 labels=None, duo=(0, 0)):
+                 labels=None, duo=(0, 0), kv0=0, hkv_loc=None):
     """Time the fp64 oracle (as it stands) on this box's host cores on a bounded sample of the same
     workload: rows of layer 0's last timed prefill chunk; also check those rows against the GPU.
     With duo labels (NEXT-3) the sampled streaming heads use the duo oracle."""
@@ -512,14 +532,16 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
     oracle.build()
     g = hq // hkv
     c = sample_out0.shape[0]
-    heads = list(range(min(2, hkv)))   # kv heads sampled (q heads of their groups)
-    strm = {h: bool(labels is not None and labels[0][h]) for h in range(hkv)}
+    own = list(range(kv0, kv0 + (hkv if hkv_loc is None else hkv_loc)))  # global kv heads held in sample_out0
+    heads = own[:2]                    # kv heads sampled (q heads of their groups)
+    strm = {h: bool(labels is not None and labels[0][h]) for h in own}
     if labels is not None:             # one retrieval and one streaming head when both exist
-        r_h = [h for h in range(hkv) if not strm[h]][:1]
-        s_h = [h for h in range(hkv) if strm[h]][:1]
+        r_h = [h for h in own if not strm[h]][:1]
+        s_h = [h for h in own if strm[h]][:1]
         heads = (r_h + s_h) or heads
     kv = {h: _oracle_inputs_for_head(0, h, dec_pos + 1, d, torch) for h in heads}
-    qpre = synth.gen_block(SEED, 0, DIST, 0, 0, hq, chunk_pos, c, d)
+    q0 = own[0] * g                    # q heads of the owned kv heads only
+    qpre = synth.gen_block(SEED, 0, DIST, 0, q0, len(own) * g, chunk_pos, c, d)
     # calibrate: one row per thread
     cores = oracle.num_threads()
     rng = np.random.default_rng(0)
@@ -532,7 +554,7 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
     k0, v0 = kv[heads[0]]
     probe_t = rows_for(cores)
     t0 = time.time()
-    _oracle_rows(oracle, qpre[probe_t, heads[0] * g], chunk_pos + probe_t, k0, v0, strm[heads[0]], duo)
+    _oracle_rows(oracle, qpre[probe_t, heads[0] * g - q0], chunk_pos + probe_t, k0, v0, strm[heads[0]], duo)
     rows_per_s = len(probe_t) / max(time.time() - t0, 1e-9)
     n_tok = int(max(2, min(c, budget_s * rows_per_s / (g * len(heads)))))
     toks = rows_for(n_tok)
@@ -542,22 +564,22 @@ def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d,
     for h in heads:
         k, v = kv[h]
         for j in range(h * g, (h + 1) * g):
-            ref = _oracle_rows(oracle, qpre[toks, j], chunk_pos + toks, k, v, strm[h], duo)
-            err = np.abs(got[toks, j] - ref)
+            ref = _oracle_rows(oracle, qpre[toks, j - q0], chunk_pos + toks, k, v, strm[h], duo)
+            err = np.abs(got[toks, j - q0] - ref)
             maxerr = max(maxerr, float(err.max()))
             sumerr += float(err.sum())
             cnt += err.size
             rows += len(toks)
     el = time.time() - t0
     # decode row: the last timed decode token, sampled kv heads
-    qd = synth.gen_block(SEED, 0, DIST, 0, 0, hq, dec_pos, 1, d)[0]
+    qd = synth.gen_block(SEED, 0, DIST, 0, q0, len(own) * g, dec_pos, 1, d)[0]
     dgot = dec_sample.float().cpu().numpy()
     dmax = 0.0
     for h in heads:
         k, v = kv[h]
         for j in range(h * g, (h + 1) * g):
-            ref = _oracle_rows(oracle, qd[j:j + 1], np.array([dec_pos]), k, v, strm[h], duo)[0]
-            dmax = max(dmax, float(np.abs(dgot[j] - ref).max()))
+            ref = _oracle_rows(oracle, qd[j - q0:j - q0 + 1], np.array([dec_pos]), k, v, strm[h], duo)[0]
+            dmax = max(dmax, float(np.abs(dgot[j - q0] - ref).max()))
     rows_per_tok = L * hq
     cpu = {"value": round(rows / el / rows_per_tok, 6), "unit": "tok/s", "cores": cores, "kind": "oracle",
            "sample": f"{rows} (layer 0, q head, position) rows of the last timed prefill chunk at positions "
@@ -666,6 +688,9 @@ def main():
                          "(synthetic labels; the paper's extension table uses 0.5)")
     ap.add_argument("--duo-sink", type=int, default=64, help="NEXT-3: attention-sink tokens of streaming heads")
     ap.add_argument("--duo-window", type=int, default=256, help="NEXT-3: recent-window tokens of streaming heads")
+    ap.add_argument("--emulate-shard", type=lambda x: tuple(int(v) for v in x.split("/")), default=None,
+                    metavar="R/W", help="run rank R's head shard of a W-GPU job alone on this GPU (configs[3]/[4] "
+                                        "on one B200: e.g. --workload 70B-1M --emulate-shard 0/8)")
     ap.add_argument("--ranks-share-gpu", action="store_true",
                     help="validation only: every rank uses cuda:0 and the output gather goes through gloo")
     args = ap.parse_args()

@@ -1,0 +1,70 @@
+"""bench.py's JSON contract, run as the driver runs it (a subprocess printing one JSON line).
+
+CPU: the reference arm (`--impl reference`, the fp64 oracle on host cores) on the tiny workload.
+GPU: the tiny workload through the product path, at N=1 and as one rank's share of a head-sharded
+job (`--emulate-shard 1/2`: kv head 1 and its q heads only), checking the keys the driver reads
+and the sampled parity against the oracle."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run_bench(*args, timeout=600):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT, capture_output=True,
+                       text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    res = run_bench("--impl", "reference", "--workload", "tiny", "--steps", "2", "--warmup", "3")
+    assert res["impl"] == "reference"
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert k in res, k
+    assert res["value"] > 0 and res["steps"] == 2
+    assert res["cpu_baseline"]["kind"] == "oracle" and res["cpu_baseline"]["cores"] >= 1
+    assert res["e2e"]["h2d_bytes_per_step"] == 0 and res["e2e"]["d2h_bytes_per_step"] == 0
+    assert res["config"]["workload"] == "tiny"
+
+
+def _check_ours(res):
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks",
+              "gpu_launches", "decode", "parity_sample"):
+        assert k in res, k
+    assert res["value"] > 0 and res["gpu_launches"] > 0
+    rl = res["roofline"]
+    assert rl["bound"] == "tensor" and rl["unit"] == "TFLOP/s" and rl["achieved"] > 0
+    assert abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-3
+    ps = res["parity_sample"]
+    assert ps["prefill_rows"] > 0 and ps["prefill_max_abs"] <= 2e-2 and ps["prefill_mean_abs"] <= 2e-3
+    assert ps["decode_max_abs"] <= 2e-2
+    assert res["e2e"]["h2d_bytes_per_step"] > 0 and res["e2e"]["d2h_bytes_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_tiny_contract():
+    res = run_bench("--workload", "tiny", "--steps", "2", "--warmup", "3")
+    _check_ours(res)
+    assert res["config"]["workload"] == "tiny" and res["n_gpus"] == 1
+    assert "shard_emulation" not in res
+
+
+@pytest.mark.gpu
+def test_bench_emulated_shard():
+    """Rank 1 of a 2-way head shard run alone: kv head 1 (global) and q heads 2, 3 of the tiny config; the
+    sampled rows are checked against the oracle at their GLOBAL head indices."""
+    res = run_bench("--workload", "tiny", "--steps", "2", "--warmup", "3", "--emulate-shard", "1/2")
+    _check_ours(res)
+    em = res["shard_emulation"]
+    assert em["rank"] == 1 and em["world"] == 2 and em["kv_heads"] == [1, 2] and em["q_heads"] == [2, 4]
+    assert "rank 1 of head-shard2" in res["config"]["parallelism"]
+    assert res["residency"]["host_store_bytes"] >= 1 * 1 * 2 * 1024 * 64 * 2   # 1 layer x 1 kv head (K+V)
