@@ -47,6 +47,11 @@ constexpr int NS = 2;              // K/V pipeline stages
 #define HI_SPEC_EXP 0  // measured: no gain (profiles/ab_prefill_r01.txt)
 #endif
 constexpr bool SPEC_EXP = HI_SPEC_EXP != 0;
+// Speculative first half on the split schedule (the tile max off the critical path), see the softmax.
+#ifndef HI_SPEC_SPLIT
+#define HI_SPEC_SPLIT 0
+#endif
+constexpr bool SPEC_SPLIT = HI_SPEC_SPLIT != 0;
 // SPLIT softmax warps per TMEM lane quarter and tile, each owning BN/SPLIT S columns of its rows
 // (and D/SPLIT O columns).  MUFU ex2 issues at 4 lanes/clk/SMSP (profiles/ubench_xu_rate_r01.txt), so
 // with one softmax warp per SMSP and tile the exponentials of a 128 x 128 tile alone take 1024 cycles
@@ -112,6 +117,9 @@ constexpr int P_COL = SPLIT_S_LO ? 64 : 0;    // first packed P column
 #endif
 constexpr int KS = HI_P_SPLIT_KEYS;
 static_assert(KS == 64 || KS == 96, "P split at 64 or 96 keys");
+static_assert(SPLIT == 1 || !SPLIT_S || (KS == 64 && !SPLIT_S_LO), "two warps per row split P at their 64-key boundary");
+static_assert(!SPEC_SPLIT || (KS == 64 && HI_SPLIT_S == 2),
+              "the speculative first half covers keys [0, 64) + [64, 128) of one warp's 128-column row");
 
 using namespace ptx;
 
@@ -215,10 +223,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(bar_s(t), 1);
-            mbar_init(bar_p(t), 128 * SPLIT);
+            // split P release with two warps per row (SPLIT == 2): hf = 0 and hf = 1 both arrive on p_lo, only
+            // hf = 1 on p_full (see the softmax)
+            mbar_init(bar_p(t), (SPLIT_S && SPLIT == 2) ? 128 : 128 * SPLIT);
             mbar_init(bar_o(t), 1);
             mbar_init(bar_sc(t), 128);
-            mbar_init(bar_pl(t), 128);
+            mbar_init(bar_pl(t), 128 * SPLIT);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -447,12 +457,199 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int i = 0; i < HN; ++i)
                         if (key0 + i <= lo) x[i] = __float_as_uint(-CUDART_INF_F);
                 }
-                if constexpr (SPLIT_S) {
+                if constexpr (SPLIT_S && SPLIT == 2) {
+                    // Two softmax warps per TMEM lane quarter and tile: this warp owns keys [64 hf, 64 hf + 64) of
+                    // its 32 rows and packs their P into columns [32 hf, 32 hf + 32).  The partner warp (same
+                    // tile and lane quarter, other hf) is met at a 64-thread named barrier to combine the row max.
+                    // hf = 0's P release opens PV(j)_lo, hf = 1's opens PV(j)_hi.  PV(j)_lo accumulates into
+                    // every O column, so bar_pl also takes hf = 1's arrival once its O columns are rescaled.
+                    const uint32_t pair_bar = 3 + tt * 4 + wq;
+                    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+                    const f2 sc2{sc, sc};
+                    f2 nm2{0.f, 0.f};
+                    auto exp_keys = [&]() {
+#pragma unroll
+                        for (int i = 0; i < HN; i += 2) {
+                            const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
+                            const f2 pp{ex2(a.x), ex2(a.y)};
+                            acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
+                            x[i / 2] = pack_bf16(pp.x, pp.y);
+                        }
+                    };
+                    auto half_max = [&]() {  // 4 chains: the register budget is 96 per thread at SPLIT == 2
+                        float mk[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) mk[c] = __uint_as_float(x[c]);
+#pragma unroll
+                        for (int i = 4; i < HN; i += 4)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) mk[c] = fmaxf(mk[c], __uint_as_float(x[i + c]));
+                        return fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3]));
+                    };
+                    auto row_max = [&](float mine) {  // combine with the partner warp's half
+                        *x_mine = mine;
+                        named_bar_sync(pair_bar, 64);
+                        return fmaxf(mine, *x_other);
+                    };
+                    bool spec_ok = false;
+                    float mx_row;
+                    // both warps of the pair hold the same m_run per row, so they take the same branch
+                    if (SPEC_SPLIT && __all_sync(0xffffffffu, m_run != -CUDART_INF_F)) {
+                        // speculative: exponentiate against the current reference while the max is reduced in
+                        // the MUFU shadow (exact unless a row max grows by > 2^8, see the SPLIT == 1 path)
+                        nm2 = f2{-m_run, -m_run};
+                        float mk[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) mk[c] = __uint_as_float(x[c]);
+#pragma unroll
+                        for (int i = 0; i < HN; i += 2) {
+                            if (i >= 4) {
+                                mk[i & 3] = fmaxf(mk[i & 3], __uint_as_float(x[i]));
+                                mk[(i + 1) & 3] = fmaxf(mk[(i + 1) & 3], __uint_as_float(x[i + 1]));
+                            }
+                            const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
+                            const f2 pp{ex2(a.x), ex2(a.y)};
+                            acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
+                            x[i / 2] = pack_bf16(pp.x, pp.y);
+                        }
+                        mx_row = row_max(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])));
+                        spec_ok = !__any_sync(0xffffffffu, mx_row * sc > m_run + RESCALE_THRESHOLD);
+                        if (!spec_ok) {
+                            // re-read the raw scores the packing overwrote (no P is stored yet: hf = 1 writes
+                            // columns 32-63, hf = 0's scores, only after the second pair barrier)
+                            acc[0] = acc[1] = acc[2] = acc[3] = f2{0.f, 0.f};
+#pragma unroll
+                            for (int cb = 0; cb < HN / 32; ++cb)
+                                tmem_ld32(t_s + hf * HN + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[cb * 32]));
+                            tmem_wait_ld();
+                            if (need_mask) {
+                                const int64_t lim = causal ? qpos - p.k_pos0 : static_cast<int64_t>(p.n_k) - 1;
+                                const int64_t lim2 = lim < p.n_k - 1 ? lim : static_cast<int64_t>(p.n_k) - 1;
+#pragma unroll
+                                for (int i = 0; i < HN; ++i)
+                                    if (key0 + i > lim2) x[i] = __float_as_uint(-CUDART_INF_F);
+                            }
+                            if (band && p.k_pos0 + kt0 <= p.q_pos0 + t_hi_tile - p.win) {
+                                const int64_t lo = qpos - p.win - p.k_pos0;
+#pragma unroll
+                                for (int i = 0; i < HN; ++i)
+                                    if (key0 + i <= lo) x[i] = __float_as_uint(-CUDART_INF_F);
+                            }
+                            named_bar_sync(pair_bar, 64);
+                        }
+                    } else {
+                        mx_row = row_max(half_max());
+                    }
+                    HI_TR(ttr + 1, j);
+                    float mref = m_run, alp = 1.f;
+                    if (!spec_ok) {
+                        const float mxs = mx_row * sc;
+                        const bool grw = (mx_row != -CUDART_INF_F) && (m_run == -CUDART_INF_F || mxs > m_run + RESCALE_THRESHOLD);
+                        mref = grw ? mxs : m_run;
+                        alp = grw ? ((m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mxs)) : 1.f;
+                        if ((!first || j > 0) && __any_sync(0xffffffffu, grw)) {  // this warp's O columns
+#pragma unroll 1
+                            for (int cb = 0; cb < HD / 16; ++cb) {  // 16 columns at a time: x[] is live (96 regs)
+                                uint32_t v[16];
+                                tmem_ld16(t_o + cb * 16, v);
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alp);
+                                tmem_st16(t_o + cb * 16, v);
+                            }
+                        }
+                        nm2 = (mref == -CUDART_INF_F) ? f2{0.f, 0.f} : f2{-mref, -mref};
+                    }
+                    if (hf == 1) {  // O columns [64, 128) rescaled: PV(j)_lo may accumulate
+                        tmem_wait_st();
+                        tc_fence_before();
+                        mbar_arrive(bar_pl(tt));
+                    }
+                    if (!spec_ok) exp_keys();
+                    tmem_st32(t_s + hf * (HN / 2), *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(hf == 0 ? bar_pl(tt) : bar_p(tt));
+                    HI_TR(ttr + 4, j);
+                    const f2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+                    l_run = l_run * alp + ((s01.x + s01.y) + (s23.x + s23.y));
+                    m_run = mref;
+                    continue;
+                }
+                if constexpr (SPLIT_S && SPLIT == 1) {
                     if constexpr (SPLIT_S_LO) {  // S(j) is in registers: columns 0-63 may take S(j+1)_lo
                         tc_fence_before();
                         mbar_arrive(bar_sc(tt));
                     }
+                    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+                    f2 sc2{sc, sc}, nm2{0.f, 0.f};
+                    // exponentials of keys [LO, HI) packed in place (x[i/2]); compile-time bounds keep x[] in
+                    // registers
+                    auto exp_keys = [&](auto lo_c, auto hi_c) {
+                        constexpr int LO = decltype(lo_c)::value, HI = decltype(hi_c)::value;
+#pragma unroll
+                        for (int i = LO; i < HI; i += 2) {
+                            const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
+                            const f2 pp{ex2(a.x), ex2(a.y)};
+                            acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
+                            x[i / 2] = pack_bf16(pp.x, pp.y);
+                        }
+                    };
                     float mk[8];
+                    bool spec_ok = false;
+                    if constexpr (SPEC_SPLIT) {
+                        // Speculative first half: exponentiate keys [0, KS) against the CURRENT reference max
+                        // while the tile max over all keys is reduced in the MUFU shadow, so the max is off the
+                        // critical path.  Exact whenever no row max grows by > 2^8 (the lazy-rescale rule): then
+                        // the reference would not have moved anyway.  Otherwise (rare after the first tiles) the
+                        // raw scores of keys [0, KS/2) that the packing overwrote are re-read from TMEM (S is
+                        // intact: no P has been stored yet) and the tile takes the normal path.
+                        if (__all_sync(0xffffffffu, m_run != -CUDART_INF_F)) {
+                            nm2 = f2{-m_run, -m_run};
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) mk[c] = fmaxf(__uint_as_float(x[c]), __uint_as_float(x[KS + c]));
+#pragma unroll
+                            for (int i = 0; i < KS; i += 2) {
+                                if (i >= 8) mk[i & 7] = fmaxf(mk[i & 7], __uint_as_float(x[i]));
+                                if (i + 1 >= 8) mk[(i + 1) & 7] = fmaxf(mk[(i + 1) & 7], __uint_as_float(x[i + 1]));
+                                if (KS + i >= KS + 8 && KS + i < HN) mk[(KS + i) & 7] = fmaxf(mk[(KS + i) & 7], __uint_as_float(x[KS + i]));
+                                if (KS + i + 1 >= KS + 8 && KS + i + 1 < HN)
+                                    mk[(KS + i + 1) & 7] = fmaxf(mk[(KS + i + 1) & 7], __uint_as_float(x[KS + i + 1]));
+                                const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
+                                const f2 pp{ex2(a.x), ex2(a.y)};
+                                acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
+                                x[i / 2] = pack_bf16(pp.x, pp.y);
+                            }
+#pragma unroll
+                            for (int i = 2 * KS; i < HN; i += 8)  // keys beyond 2*KS (KS = 64: none)
+#pragma unroll
+                                for (int c = 0; c < 8; ++c) mk[c] = fmaxf(mk[c], __uint_as_float(x[i + c]));
+                            const float mxs0 = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
+                                                     fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7]))) * sc;
+                            spec_ok = !__any_sync(0xffffffffu, mxs0 > m_run + RESCALE_THRESHOLD);
+                            HI_TR(ttr + 1, j);
+                            if (!spec_ok) {
+                                acc[0] = acc[1] = acc[2] = acc[3] = f2{0.f, 0.f};
+                                tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                                tmem_wait_ld();
+                                if (need_mask) {
+                                    const int64_t lim = causal ? qpos - p.k_pos0 : static_cast<int64_t>(p.n_k) - 1;
+                                    const int64_t lim2 = lim < p.n_k - 1 ? lim : static_cast<int64_t>(p.n_k) - 1;
+#pragma unroll
+                                    for (int i = 0; i < 32; ++i)
+                                        if (key0 + i > lim2) x[i] = __float_as_uint(-CUDART_INF_F);
+                                }
+                                if (band && p.k_pos0 + kt0 <= p.q_pos0 + t_hi_tile - p.win) {
+                                    const int64_t lo = qpos - p.win - p.k_pos0;
+#pragma unroll
+                                    for (int i = 0; i < 32; ++i)
+                                        if (key0 + i <= lo) x[i] = __float_as_uint(-CUDART_INF_F);
+                                }
+                            }
+                        }
+                    }
+                    float mref = m_run, alp = 1.f;
+                    if (!spec_ok) {
 #pragma unroll
                     for (int c = 0; c < 8; ++c) mk[c] = __uint_as_float(x[c]);
 #pragma unroll
@@ -462,8 +659,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])), fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
                     const float mxs = mx * sc;
                     const bool grw = (mx != -CUDART_INF_F) && (m_run == -CUDART_INF_F || mxs > m_run + RESCALE_THRESHOLD);
-                    const float mref = grw ? mxs : m_run;
-                    const float alp = grw ? ((m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mxs)) : 1.f;
+                    mref = grw ? mxs : m_run;
+                    alp = grw ? ((m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mxs)) : 1.f;
                     HI_TR(ttr + 1, j);
                     // O correction before PV(j)_lo may accumulate (PV(j-1) is complete: S(j) was issued after it)
                     if ((!first || j > 0) && __any_sync(0xffffffffu, grw)) {
@@ -478,27 +675,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                     }
                     const float nm = (mref == -CUDART_INF_F) ? 0.f : -mref;
-                    const f2 sc2{sc, sc}, nm2{nm, nm};
-                    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-                    // exponentials of keys [LO, HI) packed in place (x[i/2]); compile-time bounds keep x[] in
-                    // registers
-                    auto exp_keys = [&](auto lo_c, auto hi_c) {
-                        constexpr int LO = decltype(lo_c)::value, HI = decltype(hi_c)::value;
-#pragma unroll
-                        for (int i = LO; i < HI; i += 2) {
-                            const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
-                            const f2 pp{ex2(a.x), ex2(a.y)};
-                            acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
-                            x[i / 2] = pack_bf16(pp.x, pp.y);
-                        }
-                    };
+                    nm2 = f2{nm, nm};
+                    }
                     auto release_p = [&](uint32_t bar) {
                         tmem_wait_st();
                         tc_fence_before();
                         mbar_arrive(bar);
                     };
                     // keys [0, KS) -> packed columns [P_COL, P_COL + KS/2): PV(j)_lo may start
-                    exp_keys(std::integral_constant<int, 0>{}, std::integral_constant<int, KS>{});
+                    if (!spec_ok) exp_keys(std::integral_constant<int, 0>{}, std::integral_constant<int, KS>{});
                     tmem_st32(t_s + P_COL, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
                     if constexpr (KS == 96) tmem_st16(t_s + P_COL + 32, &x[32]);
                     release_p(bar_pl(tt));
