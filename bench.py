@@ -462,6 +462,7 @@ def run_ours(args, rank, world, local_rank, pg):
         "clocks": clk,
         "gpu_launches": launches,
         "residency": {"staging_bytes": st1["staging_bytes"], "staging_bound_bytes": st1["staging_bound_bytes"],
+                      "one_head_bytes": 4 * d * max_ctx,
                       "head_group": st1["head_group"],
                       "host_store_bytes": st1["host_store_bytes"], "init_s": round(init_s, 2),
                       "resident_kv_heads": st1["resident_kv_heads"], "resident_bytes": st1["resident_bytes"]},

@@ -55,8 +55,9 @@ typedef enum {
  * Any field left 0 takes the default shown. */
 typedef struct hi_options {
     int n_slots;          /* staging slots per context (default 4, min 2: "ping-pong", Fig. 4) */
-    int64_t slot_tokens;  /* tokens per slot (default floor(max_ctx/n_slots) rounded down to 64, min 64),
-                             so that n_slots*slot_tokens*4*head_dim <= one head's K+V at max_ctx (Eq. 11) */
+    int64_t slot_tokens;  /* tokens per slot and head (default floor(max_ctx/(n_slots*head_group)) rounded down
+                             to 64, min 64), so that n_slots*head_group*slot_tokens*4*head_dim <= one head's K+V
+                             at max_ctx (Eq. 11) for every head group; an explicit value is used as given */
     int device;           /* CUDA device ordinal (default: the current device) */
     int flags;            /* HI_FLAG_* bits */
     int numa_policy;      /* 0 = bind the host store to the GPU's NUMA node (sysfs), 1 = no binding,
@@ -70,8 +71,9 @@ typedef struct hi_options {
     int head_group;       /* NEXT-2 (§4 "adaptive head-wise offloading"; App. D; Tab. 5-7
                               P:L513-606): kv heads moved and computed per unit (one H2D per block carries
                               `head_group` heads; one kernel launch covers them).  Default 1 = finest
-                              head-wise offload; kv_heads/world = layer-wise offload.  Staging grows to
-                              head_group heads at max_ctx.  Must divide kv_heads/world, or be
+                              head-wise offload; kv_heads/world = layer-wise offload.  With the default
+                              slot size the staging ring stays one head's K+V at max_ctx (shorter blocks);
+                              with an explicit slot_tokens it grows head_group-fold.  Must divide kv_heads/world, or be
                               HI_GROUP_AUTO (-1): the smallest divisor whose chunk launch fills
                               >= 8 waves of 128-row tiles, staging capped at 1/32 of HBM. */
     /* NEXT-3 head-wise sparsity (duo-attention, §4; App. D; Tab. "Prefill 1M, Decoding
@@ -105,7 +107,8 @@ typedef struct hi_options {
 typedef struct hi_stats {
     int64_t host_store_bytes;     /* pinned host KV bytes (L * Hkv_loc * max_ctx * 4 * d) */
     int64_t staging_bytes;        /* device staging slots, total */
-    int64_t staging_bound_bytes;  /* head_group heads at max_ctx: 4*d*max_ctx*head_group (Eq. 11, reading R8) */
+    int64_t staging_bound_bytes;  /* one head at max_ctx, 4*d*max_ctx (Eq. 11, reading R8), with the default
+                                     slot size; head_group heads (x head_group) with an explicit slot_tokens */
     int64_t workspace_bytes;      /* other device buffers (pack, accumulators, partials) */
     int64_t h2d_bytes;            /* cumulative history bytes streamed host->device */
     int64_t d2h_bytes;            /* cumulative new-K/V bytes written back device->host */

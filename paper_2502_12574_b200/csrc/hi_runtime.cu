@@ -78,6 +78,7 @@ struct hi_ctx {
     // (b) staging
     int n_slots = 0;
     int64_t slot_tokens = 0;
+    bool slot_default = true;   // slot_tokens chosen by hi_init: the ring holds <= one head at max_ctx
     size_t slot_bytes = 0;
     int group = 1;                     // NEXT-2: kv heads per transfer + kernel unit (slot holds `group` heads)
     uint8_t* d_stage = nullptr;
@@ -495,9 +496,11 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     c->scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(head_dim)));
     c->seq_len.assign(layers, 0);
     c->n_slots = o.n_slots;
-    int64_t st = o.slot_tokens;
-    if (st == 0) st = std::max<int64_t>(64, (max_ctx / o.n_slots) / 64 * 64);
-    c->slot_tokens = st;
+    // default slot size: the whole ring (n_slots slots of `group` heads) holds at most ONE head's K+V at
+    // max_ctx (Eq. 11, reading R8), whatever the head group; an explicit slot_tokens is taken as given
+    auto default_slot_tokens = [&](int group) {
+        return std::max<int64_t>(64, (max_ctx / (static_cast<int64_t>(o.n_slots) * group)) / 64 * 64);
+    };
 
     auto bail = [&](hi_status s, const std::string& msg) {
         g_init_error = msg.empty() ? c->err : msg;
@@ -520,7 +523,9 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     // head groups (NEXT-2).  Auto: the smallest divisor G of Hkv_loc whose chunk-segment launch has >= 8
     // waves of 128-row tiles (launch fill/drain amortised, Tab. 5-7 short-context regime), while the
     // staging ring stays <= 1/32 of device memory (the adaptive memory/speed trade-off of App. D).
-    const size_t head_slot_bytes = static_cast<size_t>(st) * head_dim * 2 * 2;
+    auto head_slot_bytes_for = [&](int group) {
+        return static_cast<size_t>(o.slot_tokens ? o.slot_tokens : default_slot_tokens(group)) * head_dim * 2 * 2;
+    };
     if (o.head_group == HI_GROUP_AUTO) {
         const int64_t tiles = (static_cast<int64_t>(chunk) * g + 127) / 128;
         const int sms = prop.multiProcessorCount > 0 ? prop.multiProcessorCount : 148;
@@ -528,13 +533,17 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
         int G = 1;
         for (int cand = 1; cand <= c->Hkv_loc; ++cand) {
             if (c->Hkv_loc % cand) continue;
-            if (cand > 1 && head_slot_bytes * cand * c->n_slots > mem_cap) break;
+            if (cand > 1 && head_slot_bytes_for(cand) * cand * c->n_slots > mem_cap) break;
             G = cand;
             if (tiles * cand >= 8LL * sms) break;
         }
         o.head_group = G;
     }
     c->group = o.head_group;
+    const int64_t st = o.slot_tokens ? o.slot_tokens : default_slot_tokens(c->group);
+    c->slot_tokens = st;
+    c->slot_default = o.slot_tokens == 0;
+    const size_t head_slot_bytes = head_slot_bytes_for(c->group);
     c->slot_bytes = head_slot_bytes * c->group;
 
     // head classes: retrieval pairs numbered layer-major (cidx), streaming pairs -1 (NEXT-3)
@@ -1112,7 +1121,8 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     memset(o, 0, sizeof *o);
     o->host_store_bytes = static_cast<int64_t>(c->host_bytes);
     o->staging_bytes = static_cast<int64_t>(c->slot_bytes) * c->n_slots;
-    o->staging_bound_bytes = 4ll * c->d * c->max_ctx * c->group;  // `group` heads at max_ctx (one head: group 1)
+    // Eq. 11's one head at max_ctx for the default slot size; `group` heads when the caller sized the slots
+    o->staging_bound_bytes = 4ll * c->d * c->max_ctx * (c->slot_default ? 1 : c->group);
     o->workspace_bytes = static_cast<int64_t>(c->workspace_bytes);
     o->h2d_bytes = c->h2d_bytes;
     o->d2h_bytes = c->d2h_bytes;

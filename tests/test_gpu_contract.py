@@ -73,3 +73,18 @@ def test_init_reports_host_store_and_residency():
     assert st["n_slots"] == 3 and st["slot_tokens"] == 64
     assert st["staging_bytes"] == 3 * 64 * 4 * 64
     ctx.close()
+
+
+@pytest.mark.parametrize("group", [2, -1])
+def test_default_slots_keep_one_head_resident_with_head_groups(group):
+    """Eq. 11 (reading R8): with the default slot size the staging ring holds at most one head's K+V
+    at max_ctx whatever the head group (NEXT-2): slots shrink instead of the ring growing."""
+    from paper_2502_12574_b200.headinfer import HeadInfer
+    max_ctx, d = 4096, 128
+    ctx = HeadInfer(1, 32, 8, d, max_ctx, 1024, head_group=group)
+    st = ctx.stats()
+    one_head = 4 * d * max_ctx
+    assert st["staging_bound_bytes"] == one_head
+    assert st["staging_bytes"] <= one_head
+    assert st["slot_tokens"] * st["n_slots"] * st["head_group"] <= max_ctx
+    ctx.close()
