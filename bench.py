@@ -415,6 +415,19 @@ def run_ours(args, rank, world, local_rank, pg):
             prof = json.load(f)
         traffic = prof.get("dram_bytes_per_launch")
     launches = (st1["kernel_launches"] - st0["kernel_launches"]) + (sd1["kernel_launches"] - sd0["kernel_launches"])
+    # prefill copy engines (HI_FLAG_TIMING events on the copy streams): busy time, rate while busy, and how much
+    # of the copy time the step hides (1 = every copy overlapped with attention, SURVEY.md §8(d) timing)
+    pf_h2d_b, pf_d2h_b = st1["h2d_bytes"] - st0["h2d_bytes"], st1["d2h_bytes"] - st0["d2h_bytes"]
+    pf_h2d_ms, pf_d2h_ms = st1["h2d_copy_ms"] - st0["h2d_copy_ms"], st1["d2h_copy_ms"] - st0["d2h_copy_ms"]
+    prefill_copies = {
+        "h2d_bytes_per_step": int(pf_h2d_b / K), "d2h_bytes_per_step": int(pf_d2h_b / K),
+        "h2d_busy_ms_per_step": round(pf_h2d_ms / K, 3), "d2h_busy_ms_per_step": round(pf_d2h_ms / K, 3),
+        "h2d_gbs_while_busy": round(pf_h2d_b / (pf_h2d_ms / 1e3) / 1e9, 2) if pf_h2d_ms > 0 else None,
+        "d2h_gbs_while_busy": round(pf_d2h_b / (pf_d2h_ms / 1e3) / 1e9, 2) if pf_d2h_ms > 0 else None,
+        "h2d_busy_frac_of_step": round(pf_h2d_ms / pre_ms, 4) if pre_ms else None,
+        "attention_frac_of_step": round(pf_ms / pre_ms, 4) if pre_ms else None,
+        "copy_hidden_frac": (round(max(0.0, min(1.0, (pf_ms + pf_h2d_ms - pre_ms) / pf_h2d_ms)), 4)
+                             if pf_h2d_ms > 0 else None)}
     clk = clk_p.summary()
 
     res = {
@@ -450,6 +463,7 @@ def run_ours(args, rank, world, local_rank, pg):
                               "peak_gbs": peaks["hbm_gbs"],
                               "frac": round(dk_bytes / (dk_ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4) if dk_ms else None},
                    "clocks": clk_d.summary()},
+        "prefill_copies": prefill_copies,
         "prefill_step_roofline": {"frac": round(t_roof_pre / (pre_ms / 1e3), 4), "bound": roof_p["bound"],
                                   "t_roof_s": round(t_roof_pre, 4), "t_meas_s": round(pre_ms / 1e3, 4)},
         "roofline": {"bound": "tensor", "kernel": "prefill attention (history + causal segments)",

@@ -130,6 +130,10 @@ typedef struct hi_stats {
     int head_group;               /* kv heads per offload unit (NEXT-2) */
     int streaming_kv_heads;       /* local (layer, kv head) pairs that are duo streaming heads (NEXT-3) */
     int64_t streaming_bytes;      /* their device sink + window KV bytes */
+    /* HI_FLAG_TIMING only: copy-engine busy time, from CUDA events on the copy streams around each
+     * history block's H2D (§8(a) a3/a7) and each prefill write-back's D2H (a2) */
+    double h2d_copy_ms;
+    double d2h_copy_ms;
 } hi_stats;
 
 /*

@@ -59,7 +59,8 @@ class hi_stats(ctypes.Structure):
                 ("numa_node", ctypes.c_int), ("n_slots", ctypes.c_int), ("slot_tokens", ctypes.c_int64),
                 ("resident_kv_heads", ctypes.c_int), ("resident_bytes", ctypes.c_int64),
                 ("head_group", ctypes.c_int),
-                ("streaming_kv_heads", ctypes.c_int), ("streaming_bytes", ctypes.c_int64)]
+                ("streaming_kv_heads", ctypes.c_int), ("streaming_bytes", ctypes.c_int64),
+                ("h2d_copy_ms", ctypes.c_double), ("d2h_copy_ms", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

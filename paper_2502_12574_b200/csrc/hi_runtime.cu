@@ -40,10 +40,11 @@ namespace {
 
 thread_local std::string g_init_error = "no error";
 
+enum TimedKind { T_DECODE = 0, T_PREFILL = 1, T_H2D = 2, T_D2H = 3 };
 struct TimedLaunch {
     cudaEvent_t start, stop;
-    double work;   // algorithmic FLOPs (prefill) or bytes (decode)
-    bool prefill;
+    double work;   // algorithmic FLOPs (prefill), bytes (decode kernel) or bytes copied (H2D / D2H)
+    int kind;      // TimedKind
 };
 
 struct Slot {
@@ -113,7 +114,7 @@ struct hi_ctx {
     // HI_FLAG_TIMING
     std::vector<TimedLaunch> timed;
     std::vector<cudaEvent_t> ev_pool;
-    double prefill_ms = 0, prefill_flops = 0, decode_ms = 0, decode_bytes = 0;
+    double prefill_ms = 0, prefill_flops = 0, decode_ms = 0, decode_bytes = 0, h2d_ms = 0, d2h_ms = 0;
     int64_t prefill_timed = 0, decode_timed = 0;
 
     size_t pair(int layer, int h) const { return static_cast<size_t>(cidx[static_cast<size_t>(layer) * Hkv_loc + h]); }
@@ -332,6 +333,39 @@ hi_status check_call(hi_ctx* c, int layer) {
     return HI_OK;
 }
 
+cudaEvent_t pool_event(hi_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+}
+
+// Bracket a kernel launch (compute stream) or a batch of copies (a copy stream) with timing events when
+// HI_FLAG_TIMING is set.  On a copy stream the start event is recorded after the stream's waits, so the
+// elapsed time is the copy engine's busy time for those bytes.
+struct LaunchTimer {
+    hi_ctx* c;
+    cudaStream_t st;
+    cudaEvent_t start = nullptr;
+    LaunchTimer(hi_ctx* ctx, cudaStream_t s = nullptr) : c(ctx), st(s ? s : ctx->s_comp) {
+        if (c->flags & HI_FLAG_TIMING) {
+            start = pool_event(c);
+            if (start) cudaEventRecord(start, st);
+        }
+    }
+    void done(double work, int kind) {
+        if (!start) return;
+        cudaEvent_t stop = pool_event(c);
+        if (!stop) return;
+        cudaEventRecord(stop, st);
+        c->timed.push_back({start, stop, work, kind});
+    }
+};
+
 // Enqueue the H2D of history block [k0, k0+nk) of the kv heads `heads` of `layer` into the next slot (head
 // heads[gh] at slot position gh); the compute stream is made to wait for it.  Returns the slot through *slot_out.
 hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64_t k0, int64_t nk, int* slot_out) {
@@ -345,10 +379,12 @@ hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64
         ++c->launches;
     }
     const size_t bytes = static_cast<size_t>(nk) * c->d * 2;
+    LaunchTimer tm(c, c->s_h2d);
     for (int gh = 0; gh < nh; ++gh) {
         HI_CK(c, cudaMemcpyAsync(c->slot_k(s, gh), c->host_k(layer, heads[gh], k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
         HI_CK(c, cudaMemcpyAsync(c->slot_v(s, gh), c->host_v(layer, heads[gh], k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
     }
+    tm.done(static_cast<double>(2 * bytes) * nh, T_H2D);
     HI_CK(c, cudaEventRecord(sl.ready, c->s_h2d));
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, sl.ready, 0));  // RAW: block landed
     c->h2d_bytes += static_cast<int64_t>(2 * bytes) * nh;
@@ -361,42 +397,16 @@ hi_status release_slot(hi_ctx* c, int s) {
     return HI_OK;
 }
 
-cudaEvent_t pool_event(hi_ctx* c) {
-    if (!c->ev_pool.empty()) {
-        cudaEvent_t e = c->ev_pool.back();
-        c->ev_pool.pop_back();
-        return e;
-    }
-    cudaEvent_t e = nullptr;
-    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
-    return e;
-}
-
-// Bracket a kernel launch with timing events when HI_FLAG_TIMING is set.
-struct LaunchTimer {
-    hi_ctx* c;
-    cudaEvent_t start = nullptr;
-    LaunchTimer(hi_ctx* ctx) : c(ctx) {
-        if (c->flags & HI_FLAG_TIMING) {
-            start = pool_event(c);
-            if (start) cudaEventRecord(start, c->s_comp);
-        }
-    }
-    void done(double work, bool prefill) {
-        if (!start) return;
-        cudaEvent_t stop = pool_event(c);
-        if (!stop) return;
-        cudaEventRecord(stop, c->s_comp);
-        c->timed.push_back({start, stop, work, prefill});
-    }
-};
-
 void resolve_timing(hi_ctx* c) {
     for (auto& t : c->timed) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, t.start, t.stop) == cudaSuccess) {
-            if (t.prefill) { c->prefill_ms += ms; c->prefill_flops += t.work; ++c->prefill_timed; }
-            else { c->decode_ms += ms; c->decode_bytes += t.work; ++c->decode_timed; }
+            switch (t.kind) {
+                case T_PREFILL: c->prefill_ms += ms; c->prefill_flops += t.work; ++c->prefill_timed; break;
+                case T_DECODE: c->decode_ms += ms; c->decode_bytes += t.work; ++c->decode_timed; break;
+                case T_H2D: c->h2d_ms += ms; break;
+                default: c->d2h_ms += ms; break;
+            }
         }
         c->ev_pool.push_back(t.start);
         c->ev_pool.push_back(t.stop);
@@ -678,6 +688,8 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     // heads (NEXT-3) keep only their sink + window on the GPU (appended after their attention below)
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
     const size_t row_bytes = static_cast<size_t>(d) * 2;
+    LaunchTimer tm_wb(c, c->s_d2h);
+    const int64_t wb0 = c->d2h_bytes;
     for (int h = 0; h < Hkv; ++h) {
         if (c->streaming(layer, h)) continue;
         const __nv_bfloat16* pk = c->d_pack + (static_cast<size_t>(h) * 2 + 0) * n * d;
@@ -691,6 +703,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
         HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, s), pv, n * row_bytes, cudaMemcpyDeviceToHost, c->s_d2h));
         c->d2h_bytes += static_cast<int64_t>(2 * n * row_bytes);
     }
+    tm_wb.done(static_cast<double>(c->d2h_bytes - wb0), T_D2H);
     HI_CK(c, cudaEventRecord(c->ev_pack_free, c->s_d2h));
     HI_CK(c, cudaEventRecord(c->ev_layer_d2h[layer], c->s_d2h));
 
@@ -717,7 +730,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
         LaunchTimer tm(c);
         HI_CK(c, launch_prefill(c, p));
         if (timing)
-            tm.done(4.0 * d * g * p.n_heads * seg_pairs(s, n, p.k_pos0, p.n_k, flags & hi::PF_CAUSAL, p.win), true);
+            tm.done(4.0 * d * g * p.n_heads * seg_pairs(s, n, p.k_pos0, p.n_k, flags & hi::PF_CAUSAL, p.win), T_PREFILL);
         ++c->launches;
         return HI_OK;
     };
@@ -908,7 +921,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     auto launch = [&](const hi::DecodePartialParams& p, int nsp, int nh, int64_t nk) -> hi_status {
         LaunchTimer tm(c);
         HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, nh, c->s_comp));
-        tm.done(4.0 * d * static_cast<double>(nk) * nh, false);
+        tm.done(4.0 * d * static_cast<double>(nk) * nh, T_DECODE);
         ++c->launches;
         return HI_OK;
     };
@@ -1141,6 +1154,8 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     o->head_group = c->group;
     o->streaming_kv_heads = c->n_stream;
     o->streaming_bytes = static_cast<int64_t>(c->duo_bytes);
+    o->h2d_copy_ms = c->h2d_ms;
+    o->d2h_copy_ms = c->d2h_ms;
     o->numa_node = c->numa_node;
     o->n_slots = c->n_slots;
     o->slot_tokens = c->slot_tokens;

@@ -88,3 +88,27 @@ def test_default_slots_keep_one_head_resident_with_head_groups(group):
     assert st["staging_bytes"] <= one_head
     assert st["slot_tokens"] * st["n_slots"] * st["head_group"] <= max_ctx
     ctx.close()
+
+
+def test_timing_flag_reports_copy_engine_time():
+    """HI_FLAG_TIMING brackets every history H2D block and every prefill write-back D2H with events on the
+    copy streams: busy time > 0 and a rate below the host link's physical ceiling (PCIe 5 x16: 64 GB/s)."""
+    from paper_2502_12574_b200._lib import HI_FLAG_TIMING
+    from paper_2502_12574_b200.headinfer import HeadInfer
+    from synth.cuda import fill_
+    L, hq, hkv, d, c = 2, 32, 8, 128, 4096
+    ctx = HeadInfer(L, hq, hkv, d, 4 * c, c, flags=HI_FLAG_TIMING)
+    for i in range(4):
+        for l in range(L):
+            Q = fill_(torch.empty((c, hq, d), dtype=torch.bfloat16, device="cuda"), 1, 0, "U", l, 0, i * c)
+            K = fill_(torch.empty((c, hkv, d), dtype=torch.bfloat16, device="cuda"), 1, 1, "U", l, 0, i * c)
+            V = fill_(torch.empty((c, hkv, d), dtype=torch.bfloat16, device="cuda"), 1, 2, "U", l, 0, i * c)
+            ctx.prefill_chunk(l, Q, K, V)
+    ctx.synchronize()
+    st = ctx.stats()
+    assert st["h2d_bytes"] == L * hkv * 4 * d * c * (0 + 1 + 2 + 3)
+    assert st["d2h_bytes"] == L * hkv * 4 * d * c * 4
+    assert st["h2d_copy_ms"] > 0 and st["d2h_copy_ms"] > 0
+    assert st["h2d_bytes"] / (st["h2d_copy_ms"] / 1e3) < 64e9
+    assert st["d2h_bytes"] / (st["d2h_copy_ms"] / 1e3) < 64e9
+    ctx.close()
