@@ -75,7 +75,8 @@ typedef struct hi_options {
                               slot size the staging ring stays one head's K+V at max_ctx (shorter blocks);
                               with an explicit slot_tokens it grows head_group-fold.  Must divide kv_heads/world, or be
                               HI_GROUP_AUTO (-1): the smallest divisor whose chunk launch fills
-                              >= 8 waves of 128-row tiles, staging capped at 1/32 of HBM. */
+                              >= 8 waves of 128-row tiles, staging capped at 1/32 of HBM; or
+                              HI_GROUP_PAPER (-2): the paper's schedule by max_ctx (see below). */
     /* NEXT-3 head-wise sparsity (duo-attention, §4; App. D; Tab. "Prefill 1M, Decoding
      * with 1M KV cache" P:L988-1000): streaming_heads points at layers*kv_heads bytes (GLOBAL kv head index,
      * layer-major; the context reads its shard), nonzero = streaming head.  A streaming head is never
@@ -91,6 +92,10 @@ typedef struct hi_options {
 
 #define HI_RESIDENT_AUTO (-1)
 #define HI_GROUP_AUTO (-1)
+#define HI_GROUP_PAPER (-2)  /* head_group: the paper's context-range schedule (§4): max_ctx <= 512K ->
+                                all kv heads in one unit, <= 1M -> 2 groups, <= 2M -> 4, else 8 groups (bounds
+                                2^19/2^20/2^21 plus a 64K-token decode tail); a unit is kv_heads/groups heads,
+                                capped at this shard's kv heads */
 
 #define HI_FLAG_POISON_SLOTS 0x1 /* fill each staging slot with NaN before every H2D (race detection) */
 #define HI_FLAG_NO_HUGEPAGE 0x2  /* do not madvise(MADV_HUGEPAGE) the host store */

@@ -25,6 +25,7 @@ HI_FLAG_PREFILL_2CTA = 0x20
 HI_FLAG_PREFILL_TC1 = 0x40
 HI_RESIDENT_AUTO = -1
 HI_GROUP_AUTO = -1
+HI_GROUP_PAPER = -2
 
 # every symbol include/headinfer.h and include/hilayer.h declare (checked by tests/test_abi.py)
 EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",

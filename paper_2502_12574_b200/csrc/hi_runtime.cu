@@ -474,7 +474,8 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     if (o.n_slots == 0) o.n_slots = 4;
     if (o.head_group == 0) o.head_group = 1;
     if (o.n_slots < 2 || o.n_slots > 64 || o.slot_tokens < 0 || o.resident_kv_heads < HI_RESIDENT_AUTO ||
-        (o.head_group != HI_GROUP_AUTO && (o.head_group < 1 || (kv_heads / world) % o.head_group != 0))) {
+        (o.head_group != HI_GROUP_AUTO && o.head_group != HI_GROUP_PAPER &&
+         (o.head_group < 1 || (kv_heads / world) % o.head_group != 0))) {
         g_init_error = "invalid hi_options (n_slots in [2,64], slot_tokens >= 0, resident_kv_heads >= -1, "
                        "head_group = -1 or >= 1 dividing kv_heads/world)";
         return HI_EINVAL;
@@ -536,6 +537,18 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     auto head_slot_bytes_for = [&](int group) {
         return static_cast<size_t>(o.slot_tokens ? o.slot_tokens : default_slot_tokens(group)) * head_dim * 2 * 2;
     };
+    if (o.head_group == HI_GROUP_PAPER) {
+        // the paper's adaptive schedule (§4 "Adaptive Head-wise Offloading"; Tab. 6/7 "Adaptive"): all
+        // heads fused up to 500K tokens, 2 groups to 1M, 4 to 2M, 8 (one head per unit) beyond; the number of
+        // groups is over the model's kv heads, so this shard's unit is Hkv_loc / groups heads (at least 1)
+        // range bounds 512K / 1M / 2M tokens (2^19, 2^20, 2^21), each with a 64K-token decode tail
+        const int64_t tail = 1 << 16;
+        const int groups = max_ctx <= (1 << 19) + tail ? 1 : max_ctx <= (1 << 20) + tail ? 2
+                           : max_ctx <= (1 << 21) + tail ? 4 : 8;
+        int G = std::max(1, std::min(c->Hkv_loc, kv_heads / std::min(groups, kv_heads)));
+        while (c->Hkv_loc % G) --G;
+        o.head_group = G;
+    }
     if (o.head_group == HI_GROUP_AUTO) {
         const int64_t tiles = (static_cast<int64_t>(chunk) * g + 127) / 128;
         const int sms = prop.multiProcessorCount > 0 ? prop.multiProcessorCount : 148;

@@ -112,3 +112,18 @@ def test_timing_flag_reports_copy_engine_time():
     assert st["h2d_bytes"] / (st["h2d_copy_ms"] / 1e3) < 64e9
     assert st["d2h_bytes"] / (st["d2h_copy_ms"] / 1e3) < 64e9
     ctx.close()
+
+
+@pytest.mark.parametrize("max_ctx,world,want", [(4096, 1, 8), (600_000, 1, 4), (1_048_704, 1, 4), (1_500_000, 1, 2),
+                                                 (3_000_000, 1, 1), (600_000, 2, 4), (600_000, 8, 1),
+                                                 (1_500_000, 2, 2)])
+def test_paper_adaptive_head_groups(max_ctx, world, want):
+    """HI_GROUP_PAPER: §4 "Adaptive Head-wise Offloading" -- all heads fused up to 500K, two groups to
+    1M, four to 2M, eight (head-wise) beyond, for Llama-3-8B's 8 kv heads; a unit never spans ranks."""
+    from paper_2502_12574_b200._lib import HI_GROUP_PAPER
+    from paper_2502_12574_b200.headinfer import HeadInfer
+    ctx = HeadInfer(1, 32, 8, 64, max_ctx, 256, 0, world, head_group=HI_GROUP_PAPER, numa_policy=1)
+    st = ctx.stats()
+    assert st["head_group"] == want
+    assert st["staging_bytes"] <= 4 * 64 * max_ctx      # still one head's K+V (default slot size)
+    ctx.close()
