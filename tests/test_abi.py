@@ -79,7 +79,7 @@ def test_init_without_gpu_fails_loudly(lib):
     assert b"CUDA" in lib.hi_last_error(None) or b"device" in lib.hi_last_error(None)
 
 
-@pytest.mark.parametrize("opts", [dict(head_group=3), dict(head_group=-2), dict(n_slots=1),
+@pytest.mark.parametrize("opts", [dict(head_group=3), dict(head_group=-3), dict(n_slots=1),
                                   dict(resident_kv_heads=-2)])
 def test_init_rejects_invalid_options(lib, opts):
     """hi_init_ex validates hi_options before touching CUDA (head_group must divide kv_heads/world)."""
