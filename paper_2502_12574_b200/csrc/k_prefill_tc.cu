@@ -590,7 +590,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                         for (int i = LO; i < HI; i += 2) {
                             const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
-                            const f2 pp{ex2(a.x), ex2(a.y)};
+                            // POLY_PAIRS > 0 (experiment): that many of every 4 pairs on the FMA-pipe polynomial
+                            const f2 pp = ((i >> 1) & 3) < POLY_PAIRS ? ex2_poly2(a) : f2{ex2(a.x), ex2(a.y)};
                             acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
                             x[i / 2] = pack_bf16(pp.x, pp.y);
                         }
