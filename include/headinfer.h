@@ -106,6 +106,13 @@ typedef struct hi_options {
 #define HI_FLAG_PREFILL_2CTA 0x20     /* head_dim 128: use the CTA-pair (cta_group::2, M = 256) tcgen05 prefill
                                          kernel instead of the single-CTA one (A/B comparisons; measured slower) */
 #define HI_FLAG_PREFILL_TC1 0x40      /* use the one-tile / three-S-buffer tcgen05 prefill kernel (k_prefill_tc1.cu) */
+#define HI_FLAG_JITTER 0x80     /* hazard testing: before every history H2D block, write-back D2H and
+                                   attention launch, hold that stream for a pseudo-random 0-200 us (counter hash);
+                                   outputs must be bit-identical to a run without it */
+#define HI_FLAG_FAULT_SKIP_RAW 0x100 /* NEGATIVE CONTROL, tests only: drop the compute stream's wait on each landed
+                                        staging block (the RAW edge of Alg. 1 l.10/13) and delay the H2D stream by
+                                        2 ms per block, so attention reads slots before their bytes land; parity
+                                        must FAIL (proves the tests see a missing dependency) */
 #define HI_FLAG_MMA_SYNC_PREFILL 0x10 /* run prefill attention on the legacy mma.sync kernel instead of the
                                          tcgen05/TMEM/TMA kernel (baseline comparator for benches only) */
 

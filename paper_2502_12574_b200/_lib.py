@@ -23,6 +23,8 @@ HI_FLAG_TIMING = 0x8
 HI_FLAG_MMA_SYNC_PREFILL = 0x10
 HI_FLAG_PREFILL_2CTA = 0x20
 HI_FLAG_PREFILL_TC1 = 0x40
+HI_FLAG_JITTER = 0x80
+HI_FLAG_FAULT_SKIP_RAW = 0x100
 HI_RESIDENT_AUTO = -1
 HI_GROUP_AUTO = -1
 HI_GROUP_PAPER = -2

@@ -141,5 +141,6 @@ cudaError_t launch_duo_append(const DuoAppendParams& p, int d, cudaStream_t stre
 
 // ---- fill with a NaN bit pattern (poison mode, race detection) --------------------------
 cudaError_t launch_poison(void* ptr, size_t bytes, cudaStream_t stream);
+cudaError_t launch_spin(uint64_t ns, cudaStream_t stream);
 
 }  // namespace hi

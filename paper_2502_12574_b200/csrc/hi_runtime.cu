@@ -110,6 +110,7 @@ struct hi_ctx {
     std::vector<std::vector<std::vector<int>>> off_units;
     // (f) stats
     int64_t h2d_bytes = 0, d2h_bytes = 0, prefill_calls = 0, decode_calls = 0, launches = 0;
+    uint64_t jitter_ctr = 0;   // HI_FLAG_JITTER: counter of the delay hash
     double init_seconds = 0.0;
     // HI_FLAG_TIMING
     std::vector<TimedLaunch> timed;
@@ -366,6 +367,19 @@ struct LaunchTimer {
     }
 };
 
+// HI_FLAG_JITTER: hold `s` for a pseudo-random 0-200 us (splitmix64 of a per-context counter), so the three
+// streams complete in orders a plain run never produces; every dependency is an event, so outputs must not change.
+hi_status jitter(hi_ctx* c, cudaStream_t s) {
+    if (!(c->flags & HI_FLAG_JITTER)) return HI_OK;
+    uint64_t z = (++c->jitter_ctr) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    HI_CK(c, hi::launch_spin(z % 200000, s));
+    ++c->launches;
+    return HI_OK;
+}
+
 // Enqueue the H2D of history block [k0, k0+nk) of the kv heads `heads` of `layer` into the next slot (head
 // heads[gh] at slot position gh); the compute stream is made to wait for it.  Returns the slot through *slot_out.
 hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64_t k0, int64_t nk, int* slot_out) {
@@ -374,6 +388,11 @@ hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64
     c->next_slot = (c->next_slot + 1) % c->n_slots;
     Slot& sl = c->slots[s];
     HI_CK(c, cudaStreamWaitEvent(c->s_h2d, sl.free_, 0));  // WAR: previous consumer of this slot done
+    if (hi_status js = jitter(c, c->s_h2d); js != HI_OK) return js;
+    if (c->flags & HI_FLAG_FAULT_SKIP_RAW) {  // negative control: the block lands 2 ms late
+        HI_CK(c, hi::launch_spin(2000000, c->s_h2d));
+        ++c->launches;
+    }
     if (c->flags & HI_FLAG_POISON_SLOTS) {
         HI_CK(c, hi::launch_poison(c->slot_k(s), c->slot_bytes, c->s_h2d));
         ++c->launches;
@@ -386,7 +405,8 @@ hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64
     }
     tm.done(static_cast<double>(2 * bytes) * nh, T_H2D);
     HI_CK(c, cudaEventRecord(sl.ready, c->s_h2d));
-    HI_CK(c, cudaStreamWaitEvent(c->s_comp, sl.ready, 0));  // RAW: block landed
+    if (!(c->flags & HI_FLAG_FAULT_SKIP_RAW))
+        HI_CK(c, cudaStreamWaitEvent(c->s_comp, sl.ready, 0));  // RAW: block landed
     c->h2d_bytes += static_cast<int64_t>(2 * bytes) * nh;
     *slot_out = s;
     return HI_OK;
@@ -701,6 +721,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     // heads (NEXT-3) keep only their sink + window on the GPU (appended after their attention below)
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
     const size_t row_bytes = static_cast<size_t>(d) * 2;
+    if (hi_status js = jitter(c, c->s_d2h); js != HI_OK) return js;
     LaunchTimer tm_wb(c, c->s_d2h);
     const int64_t wb0 = c->d2h_bytes;
     for (int h = 0; h < Hkv; ++h) {
@@ -740,6 +761,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     // one launch over segment keys [k_pos0, k_pos0 + n_k) for the unit's heads
     auto run = [&](hi::PrefillParams& p, int flags) -> hi_status {
         p.flags = flags;
+        if (hi_status js = jitter(c, c->s_comp); js != HI_OK) return js;
         LaunchTimer tm(c);
         HI_CK(c, launch_prefill(c, p));
         if (timing)
@@ -899,6 +921,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     HI_CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_layer_d2h[layer], 0));
     // append (Alg. 1 line 26 "Async Update CPU KV cache"): host row s of every offloaded local kv head
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
+    if (hi_status js = jitter(c, c->s_d2h); js != HI_OK) return js;
     for (int h = 0; h < Hkv; ++h) {
         if (c->streaming(layer, h)) continue;  // NEXT-3: sink / ring append below
         if (c->resident(layer, h)) {  // H_on: append in HBM (compute stream; read by later calls only)
@@ -932,6 +955,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
         return static_cast<int>((nk + p.split_len - 1) / p.split_len);
     };
     auto launch = [&](const hi::DecodePartialParams& p, int nsp, int nh, int64_t nk) -> hi_status {
+        if (hi_status js = jitter(c, c->s_comp); js != HI_OK) return js;
         LaunchTimer tm(c);
         HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, nh, c->s_comp));
         tm.done(4.0 * d * static_cast<double>(nk) * nh, T_DECODE);

@@ -88,4 +88,20 @@ cudaError_t launch_poison(void* ptr, size_t bytes, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
+// Hazard testing (HI_FLAG_JITTER / HI_FLAG_FAULT_SKIP_RAW): one thread holds its stream for
+// `ns` nanoseconds of %globaltimer, delaying everything queued behind it on that stream.
+__global__ void spin_kernel(uint64_t ns) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
+cudaError_t launch_spin(uint64_t ns, cudaStream_t stream) {
+    spin_kernel<<<1, 1, 0, stream>>>(ns);
+    return cudaGetLastError();
+}
+
 }  // namespace hi
