@@ -22,6 +22,7 @@
 
 #include <cuda_runtime.h>
 #include <errno.h>
+#include <nvtx3/nvToolsExt.h>
 #include <linux/mempolicy.h>
 #include <math.h>
 #include <stdio.h>
@@ -367,6 +368,18 @@ struct LaunchTimer {
     }
 };
 
+// NVTX range over the host-side enqueue of a call or a staged block (tracing): visible in
+// Nsight Systems / ncu --nvtx; header-only NVTX v3, a no-op when no tool is attached.
+struct NvtxRange {
+    template <typename... A>
+    explicit NvtxRange(const char* fmt, A... a) {
+        char buf[96];
+        snprintf(buf, sizeof(buf), fmt, a...);
+        nvtxRangePushA(buf);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // HI_FLAG_JITTER: hold `s` for a pseudo-random 0-200 us (splitmix64 of a per-context counter), so the three
 // streams complete in orders a plain run never produces; every dependency is an event, so outputs must not change.
 hi_status jitter(hi_ctx* c, cudaStream_t s) {
@@ -398,6 +411,8 @@ hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64
         ++c->launches;
     }
     const size_t bytes = static_cast<size_t>(nk) * c->d * 2;
+    NvtxRange nr("hi H2D layer %d heads %d+%d keys [%lld, %lld)", layer, heads[0], nh, static_cast<long long>(k0),
+                 static_cast<long long>(k0 + nk));
     LaunchTimer tm(c, c->s_h2d);
     for (int gh = 0; gh < nh; ++gh) {
         HI_CK(c, cudaMemcpyAsync(c->slot_k(s, gh), c->host_k(layer, heads[gh], k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
@@ -705,6 +720,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     if (s + n > c->max_ctx) return set_err(c, HI_ECAPACITY, "seq_len + n_tokens exceeds max_ctx");
     cudaStream_t cs = static_cast<cudaStream_t>(cuda_stream);
     const int d = c->d, Hkv = c->Hkv_loc, g = c->g;
+    NvtxRange nr("hi_prefill_chunk layer %d s %lld n %d", layer, static_cast<long long>(s), n);
 
     HI_CK(c, cudaEventRecord(c->ev_call_in, cs));
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_call_in, 0));
@@ -908,6 +924,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     cudaStream_t cs = static_cast<cudaStream_t>(cuda_stream);
     const int d = c->d, Hkv = c->Hkv_loc, g = c->g;
     const size_t row_bytes = static_cast<size_t>(d) * 2;
+    NvtxRange nr("hi_decode layer %d s %lld", layer, static_cast<long long>(s));
 
     HI_CK(c, cudaEventRecord(c->ev_call_in, cs));
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_call_in, 0));
