@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--model", action="store_true")
     ap.add_argument("--duo", type=float, default=0.0)
     ap.add_argument("--resident-heads", type=int, default=0)
+    ap.add_argument("--head-group", type=int, default=-1, help="kv heads per offload unit (NEXT-2; -1 auto, -2 paper)")
     ap.add_argument("--shape", choices=["8B", "70B"], default="8B", help="Llama-3-8B (32 L, 32 q / 8 kv) or 70B "
                     "(80 L, 64 q / 8 kv) attention shapes")
     ap.add_argument("--emulate-shard", type=lambda x: tuple(int(v) for v in x.split("/")), default=None,
@@ -49,7 +50,7 @@ def main():
         raise SystemExit("--model runs the 8B shape at world 1")
     hq_loc, hkv_loc = hq // hw, hkv // hw
     q0h, kv0h = hr * hq_loc, hr * hkv_loc
-    opts = dict(head_group=-1, resident_kv_heads=args.resident_heads)
+    opts = dict(head_group=args.head_group, resident_kv_heads=args.resident_heads)
     if args.duo > 0:
         opts.update(streaming_heads=synth.streaming_labels(bench.SEED, L, hkv, args.duo).tolist(), duo_sink=64,
                     duo_window=256)
