@@ -55,9 +55,10 @@ typedef enum {
  * Any field left 0 takes the default shown. */
 typedef struct hi_options {
     int n_slots;          /* staging slots per context (default 4, min 2: "ping-pong", Fig. 4) */
-    int64_t slot_tokens;  /* tokens per slot and head (default floor(max_ctx/(n_slots*head_group)) rounded down
-                             to 64, min 64), so that n_slots*head_group*slot_tokens*4*head_dim <= one head's K+V
-                             at max_ctx (Eq. 11) for every head group; an explicit value is used as given */
+    int64_t slot_tokens;  /* tokens per slot and head.  Default: floor(max_ctx/(n_slots*head_group)), so that
+                             n_slots*head_group*slot_tokens*4*head_dim <= one head's K+V at max_ctx (Eq. 11
+                             P:L235) for every head group, but at least min(max_ctx/2, 32768) (short contexts:
+                             fewer, longer copies); multiples of 64.  An explicit value is used as given */
     int device;           /* CUDA device ordinal (default: the current device) */
     int flags;            /* HI_FLAG_* bits */
     int numa_policy;      /* 0 = bind the host store to the GPU's NUMA node (sysfs), 1 = no binding,
@@ -119,8 +120,9 @@ typedef struct hi_options {
 typedef struct hi_stats {
     int64_t host_store_bytes;     /* pinned host KV bytes (L * Hkv_loc * max_ctx * 4 * d) */
     int64_t staging_bytes;        /* device staging slots, total */
-    int64_t staging_bound_bytes;  /* one head at max_ctx, 4*d*max_ctx (Eq. 11, reading R8), with the default
-                                     slot size; head_group heads (x head_group) with an explicit slot_tokens */
+    int64_t staging_bound_bytes;  /* default slot size: one head at max_ctx, 4*d*max_ctx (Eq. 11, reading R8),
+                                     unless the minimum block length makes the ring larger (short contexts);
+                                     explicit slot_tokens: head_group heads at max_ctx */
     int64_t workspace_bytes;      /* other device buffers (pack, accumulators, partials) */
     int64_t h2d_bytes;            /* cumulative history bytes streamed host->device */
     int64_t d2h_bytes;            /* cumulative new-K/V bytes written back device->host */

@@ -380,6 +380,27 @@ struct NvtxRange {
     ~NvtxRange() { nvtxRangePop(); }
 };
 
+// The copies of one step (a history block of `group` heads, a write-back, a decode append) go to the copy
+// engine as ONE cudaMemcpyBatchAsync (CUDA 12.8+): one API call instead of 2 per head, which is what bounds
+// short-context decode (profiles/tab67_b200_r01.md).  Stream-ordered source access.
+struct CopyBatch {
+    std::vector<void*> dst, src;
+    std::vector<size_t> size;
+    void add(void* d, const void* s_, size_t n) {
+        dst.push_back(d);
+        src.push_back(const_cast<void*>(s_));
+        size.push_back(n);
+    }
+    cudaError_t issue(cudaStream_t st) {
+        if (dst.empty()) return cudaSuccess;
+        if (dst.size() == 1) return cudaMemcpyAsync(dst[0], src[0], size[0], cudaMemcpyDefault, st);
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        size_t attr_idx = 0, fail = 0;
+        return cudaMemcpyBatchAsync(dst.data(), src.data(), size.data(), dst.size(), &attr, &attr_idx, 1, &fail, st);
+    }
+};
+
 // HI_FLAG_JITTER: hold `s` for a pseudo-random 0-200 us (splitmix64 of a per-context counter), so the three
 // streams complete in orders a plain run never produces; every dependency is an event, so outputs must not change.
 hi_status jitter(hi_ctx* c, cudaStream_t s) {
@@ -414,10 +435,12 @@ hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64
     NvtxRange nr("hi H2D layer %d heads %d+%d keys [%lld, %lld)", layer, heads[0], nh, static_cast<long long>(k0),
                  static_cast<long long>(k0 + nk));
     LaunchTimer tm(c, c->s_h2d);
+    CopyBatch cb;
     for (int gh = 0; gh < nh; ++gh) {
-        HI_CK(c, cudaMemcpyAsync(c->slot_k(s, gh), c->host_k(layer, heads[gh], k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
-        HI_CK(c, cudaMemcpyAsync(c->slot_v(s, gh), c->host_v(layer, heads[gh], k0), bytes, cudaMemcpyHostToDevice, c->s_h2d));
+        cb.add(c->slot_k(s, gh), c->host_k(layer, heads[gh], k0), bytes);
+        cb.add(c->slot_v(s, gh), c->host_v(layer, heads[gh], k0), bytes);
     }
+    HI_CK(c, cb.issue(c->s_h2d));
     tm.done(static_cast<double>(2 * bytes) * nh, T_H2D);
     HI_CK(c, cudaEventRecord(sl.ready, c->s_h2d));
     if (!(c->flags & HI_FLAG_FAULT_SKIP_RAW))
@@ -543,9 +566,15 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     c->seq_len.assign(layers, 0);
     c->n_slots = o.n_slots;
     // default slot size: the whole ring (n_slots slots of `group` heads) holds at most ONE head's K+V at
-    // max_ctx (Eq. 11, reading R8), whatever the head group; an explicit slot_tokens is taken as given
+    // max_ctx (Eq. 11, reading R8), whatever the head group -- but a block is never shorter than
+    // min(max_ctx/2, 32768) tokens: at short contexts, where one head is a few MiB, fewer and longer copies
+    // beat the per-copy and per-launch overheads (the paper's adaptive grouping trades memory for speed
+    // there too).  An explicit slot_tokens is taken as given.
+    constexpr int64_t kMinBlock = 32768;
     auto default_slot_tokens = [&](int group) {
-        return std::max<int64_t>(64, (max_ctx / (static_cast<int64_t>(o.n_slots) * group)) / 64 * 64);
+        const int64_t one_head = (max_ctx / (static_cast<int64_t>(o.n_slots) * group)) / 64 * 64;
+        const int64_t floor_blk = std::min<int64_t>((max_ctx / 2) / 64 * 64, kMinBlock);
+        return std::max<int64_t>(64, std::max(one_head, floor_blk));
     };
 
     auto bail = [&](hi_status s, const std::string& msg) {
@@ -740,6 +769,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
     if (hi_status js = jitter(c, c->s_d2h); js != HI_OK) return js;
     LaunchTimer tm_wb(c, c->s_d2h);
     const int64_t wb0 = c->d2h_bytes;
+    CopyBatch wb;
     for (int h = 0; h < Hkv; ++h) {
         if (c->streaming(layer, h)) continue;
         const __nv_bfloat16* pk = c->d_pack + (static_cast<size_t>(h) * 2 + 0) * n * d;
@@ -749,10 +779,11 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
             HI_CK(c, cudaMemcpyAsync(c->dev_v(layer, h, s), pv, n * row_bytes, cudaMemcpyDeviceToDevice, c->s_comp));
             continue;
         }
-        HI_CK(c, cudaMemcpyAsync(c->host_k(layer, h, s), pk, n * row_bytes, cudaMemcpyDeviceToHost, c->s_d2h));
-        HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, s), pv, n * row_bytes, cudaMemcpyDeviceToHost, c->s_d2h));
+        wb.add(c->host_k(layer, h, s), pk, n * row_bytes);
+        wb.add(c->host_v(layer, h, s), pv, n * row_bytes);
         c->d2h_bytes += static_cast<int64_t>(2 * n * row_bytes);
     }
+    HI_CK(c, wb.issue(c->s_d2h));
     tm_wb.done(static_cast<double>(c->d2h_bytes - wb0), T_D2H);
     HI_CK(c, cudaEventRecord(c->ev_pack_free, c->s_d2h));
     HI_CK(c, cudaEventRecord(c->ev_layer_d2h[layer], c->s_d2h));
@@ -939,6 +970,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     // append (Alg. 1 line 26 "Async Update CPU KV cache"): host row s of every offloaded local kv head
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
     if (hi_status js = jitter(c, c->s_d2h); js != HI_OK) return js;
+    CopyBatch ap;
     for (int h = 0; h < Hkv; ++h) {
         if (c->streaming(layer, h)) continue;  // NEXT-3: sink / ring append below
         if (c->resident(layer, h)) {  // H_on: append in HBM (compute stream; read by later calls only)
@@ -948,12 +980,11 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
                                      cudaMemcpyDeviceToDevice, c->s_comp));
             continue;
         }
-        HI_CK(c, cudaMemcpyAsync(c->host_k(layer, h, s), kn + static_cast<size_t>(h) * d, row_bytes,
-                                 cudaMemcpyDeviceToHost, c->s_d2h));
-        HI_CK(c, cudaMemcpyAsync(c->host_v(layer, h, s), vn + static_cast<size_t>(h) * d, row_bytes,
-                                 cudaMemcpyDeviceToHost, c->s_d2h));
+        ap.add(c->host_k(layer, h, s), kn + static_cast<size_t>(h) * d, row_bytes);
+        ap.add(c->host_v(layer, h, s), vn + static_cast<size_t>(h) * d, row_bytes);
         c->d2h_bytes += static_cast<int64_t>(2 * row_bytes);
     }
+    HI_CK(c, ap.issue(c->s_d2h));
     HI_CK(c, cudaEventRecord(c->ev_kvnew_free[layer], c->s_d2h));
     HI_CK(c, cudaEventRecord(c->ev_layer_d2h[layer], c->s_d2h));
 
@@ -1188,8 +1219,11 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     memset(o, 0, sizeof *o);
     o->host_store_bytes = static_cast<int64_t>(c->host_bytes);
     o->staging_bytes = static_cast<int64_t>(c->slot_bytes) * c->n_slots;
-    // Eq. 11's one head at max_ctx for the default slot size; `group` heads when the caller sized the slots
-    o->staging_bound_bytes = 4ll * c->d * c->max_ctx * (c->slot_default ? 1 : c->group);
+    // default slot size: Eq. 11's one head at max_ctx, or the ring itself where the minimum block length set
+    // it (short contexts); `group` heads when the caller sized the slots
+    o->staging_bound_bytes = c->slot_default
+        ? std::max<int64_t>(4ll * c->d * c->max_ctx, static_cast<int64_t>(c->slot_bytes) * c->n_slots)
+        : 4ll * c->d * c->max_ctx * c->group;
     o->workspace_bytes = static_cast<int64_t>(c->workspace_bytes);
     o->h2d_bytes = c->h2d_bytes;
     o->d2h_bytes = c->d2h_bytes;

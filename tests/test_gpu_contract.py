@@ -78,12 +78,14 @@ def test_init_reports_host_store_and_residency():
 @pytest.mark.parametrize("group", [2, -1])
 def test_default_slots_keep_one_head_resident_with_head_groups(group):
     """Eq. 11 (reading R8): with the default slot size the staging ring holds at most one head's K+V
-    at max_ctx whatever the head group (NEXT-2): slots shrink instead of the ring growing."""
+    at max_ctx whatever the head group (NEXT-2): slots shrink instead of the ring growing (long contexts,
+    where the 32768-token minimum block does not bind)."""
     from paper_2502_12574_b200.headinfer import HeadInfer
-    max_ctx, d = 4096, 128
+    max_ctx, d = 1 << 20, 64
     ctx = HeadInfer(1, 32, 8, d, max_ctx, 1024, head_group=group)
     st = ctx.stats()
     one_head = 4 * d * max_ctx
+    assert st["head_group"] == (2 if group == 2 else 8)
     assert st["staging_bound_bytes"] == one_head
     assert st["staging_bytes"] <= one_head
     assert st["slot_tokens"] * st["n_slots"] * st["head_group"] <= max_ctx
@@ -126,4 +128,17 @@ def test_paper_adaptive_head_groups(max_ctx, world, want):
     st = ctx.stats()
     assert st["head_group"] == want
     assert st["staging_bytes"] <= 4 * 64 * max_ctx      # still one head's K+V (default slot size)
+    ctx.close()
+
+
+def test_short_context_blocks_are_long():
+    """Short contexts: blocks of at least min(max_ctx/2, 32768) tokens, so a head's history is 2 copies, not
+    n_slots * group of them; the bound reports the (small) ring."""
+    from paper_2502_12574_b200.headinfer import HeadInfer
+    max_ctx, d = 10240, 128
+    ctx = HeadInfer(1, 32, 8, d, max_ctx, 1024, head_group=8)
+    st = ctx.stats()
+    assert st["slot_tokens"] == 5120
+    assert st["staging_bytes"] == 4 * 8 * 5120 * 4 * d
+    assert st["staging_bytes"] <= st["staging_bound_bytes"]
     ctx.close()
