@@ -70,8 +70,9 @@ def test_init_reports_host_store_and_residency():
     ctx = _ctx(n_slots=3)
     st = ctx.stats()
     assert st["host_store_bytes"] == 2 * 2 * 2 * 300 * 64 * 2
-    assert st["n_slots"] == 3 and st["slot_tokens"] == 64
-    assert st["staging_bytes"] == 3 * 64 * 4 * 64
+    # one head would give 300/3 -> 64-token slots; the minimum block min(max_ctx/2, 32768) -> 128 tokens
+    assert st["n_slots"] == 3 and st["slot_tokens"] == 128
+    assert st["staging_bytes"] == 3 * 128 * 4 * 64 == st["staging_bound_bytes"]
     ctx.close()
 
 

@@ -113,7 +113,7 @@ def main():
            "context": S, "chunk": c, "chunks": len(chunk_ms), "shape": args.shape,
            "shard": ({"rank": hr, "world": hw, "note": "one rank's heads alone on one GPU; every rank of the W-GPU "
                       "job does the same work on its own heads; the output all-gather is not timed"}
-                     if hw > 1 else None), "prefill_s": round(total_s, 2),
+                     if hw > 1 else None), "prefill_s": round(total_s, 4),
            "prefill_tok_s": round(S / total_s, 1), "first_chunk_ms": round(chunk_ms[0], 1),
            "last_chunk_ms": round(chunk_ms[-1], 1),
            "decode_ms_per_token": round(sum(dec_ms[1:]) / max(1, len(dec_ms) - 1), 2) if dec_ms else None,
