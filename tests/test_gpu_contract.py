@@ -128,7 +128,13 @@ def test_paper_adaptive_head_groups(max_ctx, world, want):
     ctx = HeadInfer(1, 32, 8, 64, max_ctx, 256, 0, world, head_group=HI_GROUP_PAPER, numa_policy=1)
     st = ctx.stats()
     assert st["head_group"] == want
-    assert st["staging_bytes"] <= 4 * 64 * max_ctx      # still one head's K+V (default slot size)
+    # default slot size: one head's K+V (Eq. 11), unless the minimum block min(max_ctx/2, 32768) binds
+    # (short contexts, DESIGN.md §4 "Short contexts"), where the ring is n_slots blocks of `want` heads
+    min_blk = min((max_ctx // 2) // 64 * 64, 32768)
+    ring_at_min = st["n_slots"] * want * min_blk * 4 * 64
+    assert st["staging_bytes"] <= max(4 * 64 * max_ctx, ring_at_min)
+    if max_ctx >= 1_000_000:
+        assert st["staging_bytes"] <= 4 * 64 * max_ctx  # long contexts: one head, the rule unchanged
     ctx.close()
 
 
