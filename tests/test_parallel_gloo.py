@@ -43,9 +43,9 @@ def _worker(rank, world, port, hq, hkv, d, n, q0, result):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("hq,hkv", [(8, 4), (32, 8)])
-def test_two_rank_head_shard_gather_equals_full(hq, hkv):
-    world = 2
+@pytest.mark.parametrize("hq,hkv,world", [(8, 4, 2), (32, 8, 2), (32, 8, 4)])
+def test_two_rank_head_shard_gather_equals_full(hq, hkv, world):
+    """W = 2 (and W = 4: two kv heads per rank, the 4-GPU row of configs[2]) head shards gathered."""
     mgr = mp.Manager()
     result = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), hq, hkv, 16, 40, 10, result), nprocs=world, join=True)
