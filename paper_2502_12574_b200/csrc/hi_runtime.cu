@@ -380,24 +380,28 @@ struct NvtxRange {
     ~NvtxRange() { nvtxRangePop(); }
 };
 
-// The copies of one step (a history block of `group` heads, a write-back, a decode append) go to the copy
-// engine as ONE cudaMemcpyBatchAsync (CUDA 12.8+): one API call instead of 2 per head, which is what bounds
-// short-context decode (profiles/tab67_b200_r01.md).  Stream-ordered source access.
+// The copies of one step (a history block of `group` heads, a write-back, a decode append) are collected
+// here and issued as plain stream-ordered cudaMemcpyAsync calls; a copy whose source and destination both
+// continue the previous one is merged into it, so adjacent heads' rows go to the copy engine as one transfer.
 struct CopyBatch {
     std::vector<void*> dst, src;
     std::vector<size_t> size;
     void add(void* d, const void* s_, size_t n) {
+        if (!dst.empty() && static_cast<char*>(dst.back()) + size.back() == static_cast<char*>(d) &&
+            static_cast<const char*>(src.back()) + size.back() == static_cast<const char*>(s_)) {
+            size.back() += n;
+            return;
+        }
         dst.push_back(d);
         src.push_back(const_cast<void*>(s_));
         size.push_back(n);
     }
     cudaError_t issue(cudaStream_t st) {
-        if (dst.empty()) return cudaSuccess;
-        if (dst.size() == 1) return cudaMemcpyAsync(dst[0], src[0], size[0], cudaMemcpyDefault, st);
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        size_t attr_idx = 0, fail = 0;
-        return cudaMemcpyBatchAsync(dst.data(), src.data(), size.data(), dst.size(), &attr, &attr_idx, 1, &fail, st);
+        for (size_t i = 0; i < dst.size(); ++i) {
+            cudaError_t e = cudaMemcpyAsync(dst[i], src[i], size[i], cudaMemcpyDefault, st);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
     }
 };
 
