@@ -396,10 +396,33 @@ struct CopyBatch {
         src.push_back(const_cast<void*>(s_));
         size.push_back(n);
     }
+    // A run of equal-size copies whose sources and destinations each advance by a constant pitch (the K and V
+    // rows of consecutive heads: host pitch max_ctx rows, slot pitch slot_tokens rows) is one cudaMemcpy2DAsync.
     cudaError_t issue(cudaStream_t st) {
-        for (size_t i = 0; i < dst.size(); ++i) {
-            cudaError_t e = cudaMemcpyAsync(dst[i], src[i], size[i], cudaMemcpyDefault, st);
-            if (e != cudaSuccess) return e;
+        size_t i = 0;
+        while (i < dst.size()) {
+            size_t j = i + 1;
+            if (j < dst.size() && size[j] == size[i]) {
+                const ptrdiff_t dp = static_cast<char*>(dst[j]) - static_cast<char*>(dst[i]);
+                const ptrdiff_t sp = static_cast<char*>(src[j]) - static_cast<char*>(src[i]);
+                if (dp >= static_cast<ptrdiff_t>(size[i]) && sp >= static_cast<ptrdiff_t>(size[i])) {
+                    while (j < dst.size() && size[j] == size[i] &&
+                           static_cast<char*>(dst[j]) - static_cast<char*>(dst[j - 1]) == dp &&
+                           static_cast<char*>(src[j]) - static_cast<char*>(src[j - 1]) == sp)
+                        ++j;
+                    cudaError_t e = cudaMemcpy2DAsync(dst[i], dp, src[i], sp, size[i], j - i, cudaMemcpyDefault, st);
+                    if (e == cudaSuccess) {
+                        i = j;
+                        continue;
+                    }
+                    (void)cudaGetLastError();  // pitch out of range: fall back to one copy each
+                    j = i + 1;
+                }
+            }
+            for (; i < j; ++i) {
+                cudaError_t e = cudaMemcpyAsync(dst[i], src[i], size[i], cudaMemcpyDefault, st);
+                if (e != cudaSuccess) return e;
+            }
         }
         return cudaSuccess;
     }
