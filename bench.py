@@ -3,24 +3,36 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload auto|8B-1M|8B-128K|tiny]
 
 A "step" (ours): one pass of the hot path over one batch of synthetic input --
-  prefill step = one 18944-token chunk (148 SMs x 256 rows / g) through all 32 layers (write-back D2H, history H2D through
-                 the staging slots, causal attention over history + chunk, per layer call);
-                 the timed chunks are the LAST K chunks of the 1M prefill (the most expensive ones),
-                 the W warm-up chunks precede them; the history before them is placed in the host
-                 store untimed (hi_write_host_kv, App. E P:L1010 "preparing decoding with large context").
-  decode step  = one token through all 32 layers at context S (H2D of the whole history).
-`value` = prefill tokens/s over the timed chunks (whole job, all ranks: each token is processed by
-every rank for its heads, so scaling is strong); decode ms/token and host-link GB/s ride along.
-Inputs are generated on the GPU by synth/ (seeded, bit-identical to the oracle's generator) and are
-resident in HBM before the timed region (`value`); `e2e` re-runs the timed chunks through the public
-API from pinned HOST buffers with the H2D of Q/K/V and the D2H of `out` inside the timed region.
-Inputs per step (>= 6 GiB) exceed the 126 MB L2, so no extra flush is needed.
+  prefill step = one 18944-token chunk (148 SMs x 256 rows / g) through all 32 layers (write-back D2H, history
+                 H2D through the staging slots, causal attention over history + chunk, per layer call; at N > 1
+                 the per-layer NCCL all-gather of the head-sharded outputs).  EVERY step (warm-up and timed) is
+                 the SAME chunk, the last one of the 1M prefill (positions [S - c, S), history S - c): the layer
+                 cursors are rewound before each step, and re-running a chunk rewrites identical host bytes.  So
+                 `value` does not depend on --steps, and it is the most expensive chunk of the prefill
+                 (conservative: the paper's 516 tok/s averages all chunks of a 1M prefill).  The history
+                 below it is placed in the host store untimed (hi_write_host_kv, App. E P:L1010 "preparing
+                 decoding with large context").
+  decode step  = one token through all 32 layers at context S (H2D of the whole history), again the same
+                 position every step.
+`value` = prefill tokens/s (whole job: each token is processed by every rank for its own heads, so scaling is
+strong); decode ms/token and host-link GB/s ride along.  Inputs are generated on the GPU by synth/ (seeded,
+bit-identical to the oracle's generator) and are resident in HBM before the timed region (`value`); `e2e` re-runs
+the timed chunk through the public API from pinned HOST buffers, with each layer's Q/K/V H2D (prefetched one
+layer ahead on a side stream) and the D2H of its `out` inside the timed region.  Inputs per step (>= 6 GiB)
+exceed the 126 MB L2, so no extra flush is needed.
+
+Multi-GPU: `--gpus N` with N > 1 launched without torchrun re-executes itself under
+`torch.distributed.run` (one rank per GPU, NCCL); under torchrun each rank runs on cuda:LOCAL_RANK with its own
+context, head shard and NUMA-local host store.  NCCL init logging (NCCL_DEBUG=INFO, SUBSYS=INIT unless the caller
+set them) goes to stderr: every rank's C-level stdout is redirected to stderr so that stdout carries exactly one
+line, rank 0's JSON.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -49,10 +61,23 @@ DIST = "U"  # throughput workload
 MODEL_DIMS = (4096, 14336)
 MODEL_ROPE_THETA = 500000.0
 MODEL_RMS_EPS = 1e-5
+# parity bars (north_star; R10: relative L2 per (layer, q head) as well, since |o| ~ 1e-3 at 1M under U)
+TOL_MAX_ABS, TOL_MEAN_ABS, TOL_REL_L2 = 2e-2, 2e-3, 1e-2
+
+_JSON_FD = None   # the original stdout (fd), kept for the one JSON line
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def emit(res: dict):
+    line = (json.dumps(res) + "\n").encode()
+    if _JSON_FD is not None:
+        os.write(_JSON_FD, line)
+    else:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
 
 
 # ---------------------------------------------------------------------------------------------
@@ -91,7 +116,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -100,13 +125,14 @@ class ClockSampler:
             try:
                 sm.append(float(f[1]))
                 mx = float(f[2])
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for n, v in zip(names, f[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": statistics.median(pw) if pw else None}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -121,15 +147,18 @@ def mem_available_bytes() -> int:
     return 0
 
 
-def pick_workload(name: str, world: int, steps: int, warmup: int) -> str:
+def host_store_bytes(wl: str, world: int) -> int:
+    L, hq, hkv, d, S, c = WORKLOADS[wl]
+    return L * hkv * 4 * d * (S + 16)   # all ranks together
+
+
+def pick_workload(name: str, world: int) -> str:
     if name != "auto":
         return name
-    L, hq, hkv, d, S, c = WORKLOADS["8B-1M"]
-    need = L * (hkv // world) * 4 * d * (S + steps + warmup) + L * (hq // world + 2 * hkv // world) * c * d * 2 * 2
-    # the host store must fit with room to spare (a box driven out of memory is a strike)
-    if mem_available_bytes() >= need * world + (24 << 30):
+    # the host store (all ranks of this node) must fit with room to spare (a box driven out of memory is a strike)
+    if mem_available_bytes() >= host_store_bytes("8B-1M", world) + (24 << 30) + world * (2 << 30):
         return "8B-1M"
-    log(f"bench: MemAvailable {mem_available_bytes()/2**30:.0f} GiB < need; falling back to 8B-128K")
+    log(f"bench: MemAvailable {mem_available_bytes()/2**30:.0f} GiB too small for the 8B-1M host store; using 8B-128K")
     return "8B-128K"
 
 
@@ -167,37 +196,54 @@ def run_ours(args, rank, world, local_rank, pg):
     from paper_2502_12574_b200 import roofline as rf
     from paper_2502_12574_b200._lib import HI_FLAG_TIMING
     from paper_2502_12574_b200.headinfer import HeadInfer
+    from paper_2502_12574_b200.hostlink import bind_process_to_gpu, measure_link
     from paper_2502_12574_b200.parallel import gather_heads, shard
     from synth.cuda import fill_
 
     K, W = args.steps, args.warmup
-    wl = pick_workload(args.workload, world, K, W)
-    if world > 1:
-        # every rank must agree on the workload
-        t = torch.tensor([list(WORKLOADS).index(wl)], device="cpu" if args.ranks_share_gpu else "cuda")
+    dev = torch.device("cuda", local_rank)
+    cpu_coll = args.ranks_share_gpu   # gloo validation mode: collectives on CPU tensors
+    wl = pick_workload(args.workload, world)
+    if world > 1:   # every rank must agree on the workload
+        t = torch.tensor([list(WORKLOADS).index(wl)], device="cpu" if cpu_coll else dev)
         dist.broadcast(t, 0)
         wl = list(WORKLOADS)[int(t.item())]
     L, hq, hkv, d, S, c = WORKLOADS[wl]
     # head shard: this process's rank, or (--emulate-shard R/W) rank R of a W-GPU job run alone on this GPU
     hr, hw = (rank, world) if args.emulate_shard is None else args.emulate_shard
     sh = shard(hq, hkv, hr, hw)
-    host_need = L * (hkv // hw) * 4 * d * (S + 2 * (K + W) + 8) * (world if args.emulate_shard is None else 1)
+    node_ranks = world if args.emulate_shard is None else 1
+    host_need = host_store_bytes(wl, hw) // hw * node_ranks
     if mem_available_bytes() < host_need + (24 << 30):   # a box driven out of memory is a strike
         raise SystemExit(f"workload {wl}: host store {host_need / 2**30:.0f} GiB does not fit in MemAvailable "
                          f"{mem_available_bytes() / 2**30:.0f} GiB with a 24 GiB margin")
     hq_loc, hkv_loc, q0h, kv0h = sh["q_local"], sh["kv_local"], sh["q"][0], sh["kv"][0]
-    n_pre = W + K
-    s0 = S - K * c - W * c                   # first warm-up chunk position
-    if s0 < 0:
-        raise SystemExit(f"workload {wl}: context {S} too short for {n_pre} chunks of {c}")
-    max_ctx = S + 2 * n_pre + 8              # prefill to S, then decode steps (+ e2e re-runs)
+    p_last = S - c                            # the timed chunk: positions [S - c, S), history S - c
+    if p_last < 0:
+        raise SystemExit(f"workload {wl}: context {S} shorter than one chunk {c}")
+    max_ctx = S + 8                           # prefill to S, then decode at S (and S + 1 for parity)
     peaks = rf.load_peaks()
     shape = rf.Shape(L, hq, hkv, d)
+    locality = bind_process_to_gpu(local_rank) if torch.cuda.is_available() else {}
+
+    def barrier():
+        if world > 1:
+            dist.barrier(group=pg)
+
+    # live host-link probe, every rank at once (the decode roofline's denominator under this W-concurrency)
+    link = measure_link(local_rank, gib=0.5, reps=3, barrier=barrier if world > 1 else None)
+    if world > 1:
+        lt = torch.tensor([link["h2d_gbs"], link["d2h_gbs"], link["bidir_gbs"]], dtype=torch.float64,
+                          device="cpu" if cpu_coll else dev)
+        dist.all_reduce(lt, op=dist.ReduceOp.MIN, group=pg)
+        link_min = dict(zip(("h2d_gbs", "d2h_gbs", "bidir_gbs"), lt.tolist()))
+    else:
+        link_min = {k: link[k] for k in ("h2d_gbs", "d2h_gbs", "bidir_gbs")}
 
     resident = args.resident_heads
     if resident < 0:  # as many (layer, kv head) pairs as fit next to this bench's inputs (NEXT-1)
         free_b, _ = torch.cuda.mem_get_info()
-        inputs_b = (K + 2) * L * c * (hq_loc + 2 * hkv_loc) * d * 2 + L * c * hq_loc * d * 2
+        inputs_b = 3 * L * c * (hq_loc + 2 * hkv_loc) * d * 2 + 2 * L * c * hq_loc * d * 2
         if args.model:  # 32 layers of weights + the layer workspaces
             H, I = MODEL_DIMS
             inputs_b += L * (H * (hq + 2 * hkv) * d + H * hq * d + 3 * H * I) * 2 + c * (4 * H + 3 * I) * 2
@@ -212,27 +258,23 @@ def run_ours(args, rank, world, local_rank, pg):
                         duo_window=args.duo_window)
     t0 = time.time()
     hi = HeadInfer(L, hq, hkv, d, max_ctx, c, hr, hw, flags=HI_FLAG_TIMING, resident_kv_heads=resident,
-                   head_group=args.head_group, **duo_opts)
+                   head_group=args.head_group, device=local_rank, **duo_opts)
     init_s = time.time() - t0
     t0 = time.time()
-    fill_history(hi, L, hkv_loc, kv0h, d, s0, torch, fill_, labels, duo)
+    fill_history(hi, L, hkv_loc, kv0h, d, p_last, torch, fill_, labels, duo)
     fill_s = time.time() - t0
-    log(f"[rank {rank}] {wl}: init {init_s:.1f}s (host store {hi.stats()['host_store_bytes']/2**30:.1f} GiB), "
-        f"history fill {fill_s:.1f}s")
-    for l in range(L):
-        hi.set_seq_len(l, s0)
+    log(f"[rank {rank}] {wl}: init {init_s:.1f}s (host store {hi.stats()['host_store_bytes']/2**30:.1f} GiB, "
+        f"NUMA node {hi.stats()['numa_node']}), history fill {fill_s:.1f}s; link {link}")
 
     stream = torch.cuda.current_stream()
-    gathered = None
 
-    def barrier():
-        if world > 1:
-            dist.barrier(group=pg)
-
-    gathered0 = None
+    def rewind(pos):
+        for l in range(L):
+            hi.set_seq_len(l, pos)
 
     # ---------------- the step: attention path only (default), or whole synthetic layers (--model, NEXT-4)
     model = None
+    synth_tensor_x = 3  # synth.TENSOR_X
     if args.model:
         from paper_2502_12574_b200.layer import HeadInferLayer
         from synth.cuda import fill_matrix_, gen_layer_weights_cuda
@@ -250,144 +292,121 @@ def run_ours(args, rank, world, local_rank, pg):
                                 synth_tensor_x, 0, row0=pos)
         return [gen_layer_inputs(l, pos, n, hq_loc, hkv_loc, d, q0h, kv0h, torch, fill_) for l in range(L)]
 
-    def prefill_step(inputs, outs):
-        nonlocal gathered, gathered0
-        if model is not None:   # x flows through every layer in place; outs[0] keeps layer 0's input copy
+    outs = [torch.empty((c, hq_loc, d), dtype=torch.bfloat16, device="cuda") for _ in range(L)]
+    gathered = torch.empty((world, c, hq_loc, d), dtype=torch.bfloat16, device="cuda") if world > 1 else None
+    gathered0 = torch.empty_like(gathered) if world > 1 else None
+    x_work = None
+
+    def prefill_step(inputs):
+        nonlocal x_work
+        if model is not None:   # x flows through every layer in place: start every step from the same x
+            x_work.copy_(inputs)
             for l in range(L):
-                model.prefill_chunk(l, weights[l], inputs)
+                model.prefill_chunk(l, weights[l], x_work)
             return
         for l in range(L):
             Q, Kt, Vt = inputs[l]
             hi.prefill_chunk(l, Q, Kt, Vt, outs[l])
-            if world > 1:
-                if l == 0:
-                    gathered0 = gather_heads(outs[l], group=pg, out=gathered0)
-                else:
-                    gathered = gather_heads(outs[l], group=pg, out=gathered)
+            if world > 1:   # Alg. 1 l.15 "Concatenate" across the head shards, on the critical path
+                gather_heads(outs[l], group=pg, out=gathered0 if l == 0 else gathered)
 
-    synth_tensor_x = 3  # synth.TENSOR_X
-
-    # ---------------- prefill: W warm-up chunks, then K timed chunks (all inputs resident) -------
-    outs = [torch.empty((c, hq_loc, d), dtype=torch.bfloat16, device="cuda") for _ in range(L)]
+    # ---------------- prefill: W warm-up steps, then K timed steps, all at the last chunk [S - c, S) ------
+    step_in = make_inputs(p_last, c)
+    if model is not None:
+        x_work = torch.empty_like(step_in)
     for i in range(W):
-        inputs = make_inputs(s0 + i * c, c)
-        prefill_step(inputs, outs)
-        del inputs
-    timed_inputs = [make_inputs(s0 + (W + i) * c, c) for i in range(K)]
+        rewind(p_last)
+        prefill_step(step_in)
     hi.synchronize()
     st0 = hi.stats()
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms = []
     with ClockSampler(local_rank) as clk_p:
         e0.record(stream)
         for i in range(K):
-            prefill_step(timed_inputs[i], outs)
+            es = torch.cuda.Event(enable_timing=True)
+            es.record(stream)
+            rewind(p_last)   # host-side cursor reset; waits for the previous step (a few us of bubble)
+            prefill_step(step_in)
+            ee = torch.cuda.Event(enable_timing=True)
+            ee.record(stream)
+            step_ms.append((es, ee))
         hi.synchronize()  # drain the write-back stream too
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
     pre_ms = e0.elapsed_time(e1)
+    step_ms = [a.elapsed_time(b) for a, b in step_ms]
     st1 = hi.stats()
-    sample_out0 = outs[0].clone()     # layer 0 outputs of the last timed chunk (parity sample)
-    last_chunk_pos = s0 + (W + K - 1) * c
-    del timed_inputs
+    sample_outs = {0: outs[0].clone(), L - 1: outs[L - 1].clone()} if model is None else {}
 
-    # ---------------- decode: W warm-up tokens, then K timed tokens at context S ----------------
-    dq = [make_inputs(S + i, 1) for i in range(W + K)]
+    # ---------------- decode: W warm-up tokens, then K timed tokens, all at context S -------------------
+    dq = make_inputs(S, 1)
     dout = [torch.empty((hq_loc, d), dtype=torch.bfloat16, device="cuda") for _ in range(L)]
-    gdec = None
+    gdec = torch.empty((world, hq_loc, d), dtype=torch.bfloat16, device="cuda") if world > 1 else None
 
-    def decode_step(i):
-        nonlocal gdec
+    def decode_step():
+        rewind(S)
         if model is not None:
+            xd = dq[0].clone()
             for l in range(L):
-                model.decode(l, weights[l], dq[i][0])
+                model.decode(l, weights[l], xd)
             return
         for l in range(L):
-            q, k, v = dq[i][l]
+            q, k, v = dq[l]
             hi.decode(l, q[0], k[0], v[0], dout[l])
             if world > 1:
-                gdec = gather_heads(dout[l], group=pg, out=gdec)
+                gather_heads(dout[l], group=pg, out=gdec)
 
     for i in range(W):
-        decode_step(i)
+        decode_step()
     hi.synchronize()
     sd0 = hi.stats()
     torch.cuda.synchronize()
     barrier()
     with ClockSampler(local_rank) as clk_d:
         e0.record(stream)
-        for i in range(W, W + K):
-            decode_step(i)
+        for i in range(K):
+            decode_step()
         hi.synchronize()
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
     dec_ms = e0.elapsed_time(e1)
     sd1 = hi.stats()
-    dec_sample = dout[0].clone()
-    dec_pos = S + W + K - 1
+    dec_sample = dout[0].clone() if model is None else None
+    gdec_sample = gdec.clone() if gdec is not None else None
 
-    # ---------------- e2e: the timed prefill chunks again, inputs from pinned HOST memory --------
+    # ---------------- e2e: the timed chunk again, inputs from pinned HOST memory --------------------------
     e2e = None
     if not args.no_e2e:
-        for l in range(L):
-            hi.set_seq_len(l, s0 + W * c)
-        if model is not None:   # x in, x out (the last layer's hidden states)
-            shapes = [[(c, MODEL_DIMS[0])]]
-            out_shape = (c, MODEL_DIMS[0])
-        else:
-            shapes = [[(c, hq_loc, d), (c, hkv_loc, d), (c, hkv_loc, d)] for _ in range(L)]
-            out_shape = (c, hq_loc, d)
-        host_in = [[torch.empty(sh, dtype=torch.bfloat16).pin_memory() for sh in per] for per in shapes]
-        host_out = [torch.empty(out_shape, dtype=torch.bfloat16).pin_memory() for _ in shapes]
-        dev_in = [[torch.empty(t.shape, dtype=t.dtype, device="cuda") for t in per] for per in host_in]
-        e2e_ms = 0.0
-        h2d_b = sum(t.numel() * 2 for per in host_in for t in per)
-        d2h_b = sum(t.numel() * 2 for t in host_out)
-        for i in range(K):
-            step_in = make_inputs(s0 + (W + i) * c, c)   # untimed: this step's inputs into pinned host buffers
-            step_in = [[step_in]] if model is not None else step_in
-            for per_dev, per_host in zip(step_in, host_in):
-                for t_dev, t_host in zip(per_dev, per_host):
-                    t_host.copy_(t_dev)
-            del step_in
-            torch.cuda.synchronize()
-            barrier()
-            e0.record(stream)
-            if model is not None:
-                dev_in[0][0].copy_(host_in[0][0], non_blocking=True)
-                for l in range(L):
-                    model.prefill_chunk(l, weights[l], dev_in[0][0])
-                host_out[0].copy_(dev_in[0][0], non_blocking=True)
-            else:
-                for l in range(L):
-                    for t_dev, t_host in zip(dev_in[l], host_in[l]):
-                        t_dev.copy_(t_host, non_blocking=True)
-                    hi.prefill_chunk(l, *dev_in[l], outs[l])
-                    if world > 1:
-                        gathered = gather_heads(outs[l], group=pg, out=gathered)
-                    host_out[l].copy_(outs[l], non_blocking=True)
-            hi.synchronize()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            barrier()
-            e2e_ms += e0.elapsed_time(e1)
-        del host_in, host_out, dev_in
-        e2e = {"ms": e2e_ms, "h2d": h2d_b, "d2h": d2h_b}
+        e2e = run_e2e(hi, model, weights if model is not None else None, step_in, outs, L, c, K, W, p_last, rewind,
+                      world, pg, gathered, barrier, stream, torch)
+    del step_in
 
     # ---------------- max over ranks --------------------------------------------------------------
     times = torch.tensor([pre_ms, dec_ms, e2e["ms"] if e2e else 0.0], dtype=torch.float64,
-                         device="cpu" if args.ranks_share_gpu else "cuda")
+                         device="cpu" if cpu_coll else dev)
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX, group=pg)
     pre_ms, dec_ms, e2e_ms = times.tolist()
 
+    # ---------------- parity (and, at N = 1, the cpu baseline) on sampled rows ------------------------------
+    parity, cpu = None, None
+    if not args.no_cpu_baseline and model is None:
+        if world == 1:
+            parity, cpu = full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, torch,
+                                           labels=labels, duo=duo, kv0=kv0h, hkv_loc=hkv_loc, q0=q0h)
+        else:
+            parity = sharded_parity(gathered0, gdec_sample, p_last, S, L, hq, hkv, d, world, rank, pg, torch,
+                                    labels, duo)
+
     # ---------------- report (rank 0) -------------------------------------------------------------
     if rank != 0:
         hi.close()
-        return
+        return None
     tok_s = K * c / (pre_ms / 1e3)
     dec_ms_tok = dec_ms / K
     h2d_dec = (sd1["h2d_bytes"] - sd0["h2d_bytes"]) / K
@@ -399,15 +418,15 @@ def run_ours(args, rank, world, local_rank, pg):
     peak_t = peaks["bf16_tflops_sustained"]
     dk_bytes = sd1["decode_attn_bytes"] - sd0["decode_attn_bytes"]
     dk_ms = sd1["decode_attn_ms"] - sd0["decode_attn_ms"]
-    # step rooflines (measured peaks; sustained tensor peak inside a long step)
-    pk = dict(peaks, bf16_tflops=peak_t)
+    # step rooflines: measured peaks; sustained tensor peak inside a long step; host link measured live in this run
+    # under the same W-concurrency (min over ranks)
+    pk = dict(peaks, bf16_tflops=peak_t, **link_min)
     R = st1["resident_kv_heads"]
     dk = dict(streaming=st1["streaming_kv_heads"], n_sink=max(args.duo_sink, 0), win=args.duo_window)
-    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, last_chunk_pos - c * (K - 1) // 2, c, hw, R, **dk), pk)
-    t_roof_pre = sum(rf.step_roofline_seconds(rf.prefill_step(shape, s0 + (W + i) * c, c, hw, R, **dk), pk)["seconds"]
-                     for i in range(K))
-    dec_roofs = [rf.step_roofline_seconds(rf.decode_step(shape, S + i, hw, R, **dk), pk) for i in range(W, W + K)]
-    t_roof_dec = sum(x["seconds"] for x in dec_roofs)
+    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, p_last, c, hw, R, **dk), pk)
+    t_roof_pre = K * roof_p["seconds"]
+    roof_d = rf.step_roofline_seconds(rf.decode_step(shape, S, hw, R, **dk), pk)
+    t_roof_dec = K * roof_d["seconds"]
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "ncu_prefill_traffic.json")
     if os.path.exists(prof_path):
@@ -419,16 +438,18 @@ def run_ours(args, rank, world, local_rank, pg):
     # of the copy time the step hides (1 = every copy overlapped with attention, SURVEY.md §8(d) timing)
     pf_h2d_b, pf_d2h_b = st1["h2d_bytes"] - st0["h2d_bytes"], st1["d2h_bytes"] - st0["d2h_bytes"]
     pf_h2d_ms, pf_d2h_ms = st1["h2d_copy_ms"] - st0["h2d_copy_ms"], st1["d2h_copy_ms"] - st0["d2h_copy_ms"]
+    rank_pre_ms = pre_ms   # max over ranks (the copy statistics are rank 0's)
     prefill_copies = {
         "h2d_bytes_per_step": int(pf_h2d_b / K), "d2h_bytes_per_step": int(pf_d2h_b / K),
         "h2d_busy_ms_per_step": round(pf_h2d_ms / K, 3), "d2h_busy_ms_per_step": round(pf_d2h_ms / K, 3),
         "h2d_gbs_while_busy": round(pf_h2d_b / (pf_h2d_ms / 1e3) / 1e9, 2) if pf_h2d_ms > 0 else None,
         "d2h_gbs_while_busy": round(pf_d2h_b / (pf_d2h_ms / 1e3) / 1e9, 2) if pf_d2h_ms > 0 else None,
-        "h2d_busy_frac_of_step": round(pf_h2d_ms / pre_ms, 4) if pre_ms else None,
-        "attention_frac_of_step": round(pf_ms / pre_ms, 4) if pre_ms else None,
-        "copy_hidden_frac": (round(max(0.0, min(1.0, (pf_ms + pf_h2d_ms - pre_ms) / pf_h2d_ms)), 4)
+        "h2d_busy_frac_of_step": round(pf_h2d_ms / rank_pre_ms, 4) if rank_pre_ms else None,
+        "attention_frac_of_step": round(pf_ms / rank_pre_ms, 4) if rank_pre_ms else None,
+        "copy_hidden_frac": (round(max(0.0, min(1.0, (pf_ms + pf_h2d_ms - rank_pre_ms) / pf_h2d_ms)), 4)
                              if pf_h2d_ms > 0 else None)}
     clk = clk_p.summary()
+    per_step = sorted(step_ms)
 
     res = {
         "metric": METRIC,
@@ -449,20 +470,27 @@ def run_ours(args, rank, world, local_rank, pg):
                    "duo": ({"streaming_frac": args.duo, "streaming_kv_heads": st1["streaming_kv_heads"],
                             "sink": max(args.duo_sink, 0), "window": args.duo_window,
                             "labels": "synthetic (synth.streaming_labels)"} if args.duo > 0 else None),
-                   "parallelism": (f"head-shard{world}" if args.emulate_shard is None else
+                   "parallelism": (f"head-shard{world}" + (" (ranks share cuda:0, gloo)" if cpu_coll else "")
+                                   if args.emulate_shard is None else
                                    f"rank {hr} of head-shard{hw}, run alone on 1 GPU (no all-gather)"),
-                   "prefill_step": "1 chunk x all layers",
-                   "timed_chunk_positions": [s0 + W * c, last_chunk_pos],
-                   "decode_step": "1 token x all layers", "decode_context": [S + W, S + W + K - 1],
+                   "prefill_step": "1 chunk x all layers (+ per-layer all-gather at N > 1)",
+                   "timed_chunk": [p_last, S], "timed_chunk_note": "every warm-up and timed step re-runs the last "
+                   "chunk of the 1M prefill (cursor rewound): value is independent of --steps",
+                   "decode_step": "1 token x all layers", "decode_context": S,
                    "l2": "inputs per step > L2 (>= 6 GiB), no flush needed"},
+        "prefill_step_ms": {"min": round(per_step[0], 3), "median": round(per_step[len(per_step) // 2], 3),
+                            "max": round(per_step[-1], 3), "rank": 0},
         "decode": {"ms_per_token": round(dec_ms_tok, 3), "h2d_gbs": round(h2d_gbs, 2),
-                   "link_peak_gbs": peaks["h2d_gbs"], "link_frac": round(h2d_gbs / peaks["h2d_gbs"], 4),
-                   "roofline_frac": round(t_roof_dec / (dec_ms / 1e3), 4), "roofline_bound": dec_roofs[-1]["bound"],
+                   "link_peak_gbs": round(link_min["h2d_gbs"], 2), "link_frac": round(h2d_gbs / link_min["h2d_gbs"], 4),
+                   "link_peak_source": f"measured live in this run, {world} rank(s) copying concurrently, min over ranks",
+                   "roofline_frac": round(t_roof_dec / (dec_ms / 1e3), 4), "roofline_bound": roof_d["bound"],
                    "h2d_bytes_per_token": int(h2d_dec),
                    "kernel": {"bound": "hbm", "achieved_gbs": round(dk_bytes / (dk_ms / 1e3) / 1e9, 1) if dk_ms else None,
                               "peak_gbs": peaks["hbm_gbs"],
                               "frac": round(dk_bytes / (dk_ms / 1e3) / 1e9 / peaks["hbm_gbs"], 4) if dk_ms else None},
                    "clocks": clk_d.summary()},
+        "host_link": {"rank0": link, "min_over_ranks": link_min, "committed_1gpu": {k: v for k, v in rf.HOST_LINK.items()},
+                      "locality_rank0": {k: v for k, v in locality.items() if k != "affinity"}},
         "prefill_copies": prefill_copies,
         "prefill_step_roofline": {"frac": round(t_roof_pre / (pre_ms / 1e3), 4), "bound": roof_p["bound"],
                                   "t_roof_s": round(t_roof_pre, 4), "t_meas_s": round(pre_ms / 1e3, 4)},
@@ -470,22 +498,32 @@ def run_ours(args, rank, world, local_rank, pg):
                      "achieved": round(achieved_tflops, 2) if achieved_tflops else None,
                      "peak": peak_t, "unit": "TFLOP/s",
                      "frac": round(achieved_tflops / peak_t, 4) if achieved_tflops else None,
-                     "traffic": traffic, "launches": pf_launches,
+                     "traffic": traffic, "traffic_source": "committed ncu --set full capture of the dominant launch "
+                                                           "(profiles/ncu_prefill_traffic.json), not this run",
+                     "launches": pf_launches,
                      "flops_per_launch": pf_flops / max(pf_launches, 1),
                      "peak_source": peaks["source"] + " bf16_tflops_sustained"},
         "clocks": clk,
         "gpu_launches": launches,
         "residency": {"staging_bytes": st1["staging_bytes"], "staging_bound_bytes": st1["staging_bound_bytes"],
                       "one_head_bytes": 4 * d * max_ctx,
-                      "head_group": st1["head_group"],
+                      "head_group": st1["head_group"], "numa_node": st1["numa_node"],
                       "host_store_bytes": st1["host_store_bytes"], "init_s": round(init_s, 2),
                       "resident_kv_heads": st1["resident_kv_heads"], "resident_bytes": st1["resident_bytes"]},
     }
+    if world > 1:
+        res["nccl"] = {"backend": dist.get_backend(pg), "comm_nranks": dist.get_world_size(pg),
+                       "collective": "all_gather_into_tensor of each layer call's out (prefill and decode)",
+                       "init_log": "NCCL_DEBUG=INFO NCCL_DEBUG_SUBSYS=INIT on stderr"}
     if e2e:
         res["e2e"] = {"value": round(K * c / (e2e_ms / 1e3), 2), "unit": "tok/s",
-                      "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
-    if world > 1 and not args.no_cpu_baseline:
-        res["parity_sample"] = sharded_parity(gathered0, last_chunk_pos, L, hq, hkv, d, world, torch, labels, duo)
+                      "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                      "overlap": "layer l+1's Q/K/V H2D on a side stream under layer l's attention; out D2H on "
+                                 "another side stream"}
+    if parity is not None:
+        res["parity_sample"] = parity
+    if cpu is not None:
+        res["cpu_baseline"] = cpu
     if model is not None:
         H, I = MODEL_DIMS
         gemm_tok = L * 2.0 * (H * (hq + 2 * hkv) * d + H * hq * d + 3 * H * I)  # QKV, O, gate+up, down
@@ -499,13 +537,9 @@ def run_ours(args, rank, world, local_rank, pg):
                         "attention_share_of_prefill": round(pf_ms / pre_ms, 4) if pre_ms else None,
                         "step_roofline_frac": round((t_roof_pre + t_gemm) / (pre_ms / 1e3), 4),
                         "parity": "tests/test_gpu_layer.py (layer oracle, incl. one 8B-shaped layer)",
-                        "note": "history K/V below the timed chunks are synthetic (placed untimed), not produced "
+                        "note": "history K/V below the timed chunk are synthetic (placed untimed), not produced "
                                 "by running the layers; no embedding / LM head"}
         model.close()
-    if world == 1 and not args.no_cpu_baseline and model is None:
-        res["cpu_baseline"], res["parity_sample"] = cpu_baseline(hi, sample_out0, last_chunk_pos, dec_sample, dec_pos,
-                                                                 L, hq, hkv, d, torch, labels=labels, duo=duo,
-                                                                 kv0=kv0h, hkv_loc=hkv_loc)
     if args.emulate_shard is not None:
         res["shard_emulation"] = {
             "rank": hr, "world": hw, "kv_heads": list(sh["kv"]), "q_heads": list(sh["q"]),
@@ -514,13 +548,98 @@ def run_ours(args, rank, world, local_rank, pg):
                     "as fast as this one; the per-layer output all-gather and any host-link sharing between "
                     "ranks are not measured"}
     hi.close()
-    print(json.dumps(res), flush=True)
+    return res
+
+
+def run_e2e(hi, model, weights, step_in, outs, L, c, K, W, p_last, rewind, world, pg, gathered, barrier, stream, torch):
+    """The timed chunk through the public API from pinned HOST buffers: per step, every layer's Q/K/V go host ->
+    device (double-buffered, layer l+1's copy on a side stream under layer l's attention) and every layer's `out`
+    device -> host (side stream); both inside the timed region."""
+    from paper_2502_12574_b200.parallel import gather_heads
+    if model is not None:   # x in, x out (the last layer's hidden states)
+        host_x = step_in.cpu().pin_memory()
+        host_out = torch.empty_like(host_x).pin_memory()
+        dev_x = torch.empty_like(step_in)
+        e2e_ms = 0.0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for i in range(W + K):
+            rewind(p_last)
+            torch.cuda.synchronize()
+            barrier()
+            e0.record(stream)
+            dev_x.copy_(host_x, non_blocking=True)
+            for l in range(L):
+                model.prefill_chunk(l, weights[l], dev_x)
+            host_out.copy_(dev_x, non_blocking=True)
+            hi.synchronize()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i >= W:
+                e2e_ms += e0.elapsed_time(e1)
+        return {"ms": e2e_ms, "h2d": host_x.numel() * 2, "d2h": host_out.numel() * 2 * world}
+    host_in = [[t.cpu().pin_memory() for t in per] for per in step_in]
+    host_out = [torch.empty(outs[0].shape, dtype=torch.bfloat16).pin_memory() for _ in range(L)]
+    dev_in = [[torch.empty_like(t) for t in step_in[0]] for _ in range(2)]
+    dev_out = [torch.empty_like(outs[0]) for _ in range(2)]
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_ready = [torch.cuda.Event() for _ in range(2)]
+    ev_in_free = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_out_free = [torch.cuda.Event() for _ in range(2)]
+    h2d_b = sum(t.numel() * 2 for per in host_in for t in per)
+    d2h_b = sum(t.numel() * 2 for t in host_out) * world
+
+    def issue_in(l):
+        b = l % 2
+        s_in.wait_event(ev_in_free[b])           # layer l-2's attention has read this buffer
+        with torch.cuda.stream(s_in):
+            for t_dev, t_host in zip(dev_in[b], host_in[l]):
+                t_dev.copy_(t_host, non_blocking=True)
+        ev_ready[b].record(s_in)
+
+    for ev in ev_in_free + ev_out_free:
+        ev.record(stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_ms = 0.0
+    for i in range(W + K):
+        rewind(p_last)
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        s_in.wait_stream(stream)
+        issue_in(0)
+        for l in range(L):
+            b = l % 2
+            if l + 1 < L:
+                issue_in(l + 1)
+            stream.wait_event(ev_ready[b])
+            stream.wait_event(ev_out_free[b])    # layer l-2's out has reached the host
+            hi.prefill_chunk(l, *dev_in[b], dev_out[b])
+            ev_in_free[b].record(stream)
+            if world > 1:
+                gather_heads(dev_out[b], group=pg, out=gathered)
+            ev_done[b].record(stream)
+            s_out.wait_event(ev_done[b])
+            with torch.cuda.stream(s_out):
+                host_out[l].copy_(dev_out[b], non_blocking=True)
+            ev_out_free[b].record(s_out)
+        stream.wait_stream(s_out)
+        hi.synchronize()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= W:
+            e2e_ms += e0.elapsed_time(e1)
+    # the e2e outputs are the same chunk as the timed one: they must equal the resident-input outputs bit for bit
+    same = all(torch.equal(host_out[l], outs[l].cpu()) for l in (0, L - 1))
+    if not same:
+        log("bench: WARNING e2e outputs differ from the resident-input run")
+    return {"ms": e2e_ms, "h2d": h2d_b, "d2h": d2h_b, "bit_identical_to_resident_run": same}
 
 
 # ---------------------------------------------------------------------------------------------
-def _oracle_inputs_for_head(layer, kv_head, upto, d, torch):
-    """K, V of (layer, kv head) positions [0, upto) from synth's GPU twin (bit-identical to
-    synth.gen_block, pinned by tests) -> host numpy; the oracle never reads the library."""
+def _oracle_kv(layer, kv_head, upto, d, torch):
+    """K, V of (layer, kv head) positions [0, upto) from synth's GPU twin (bit-identical to synth.gen_block,
+    pinned by tests) -> host numpy; the oracle never reads the library."""
     import numpy as np
     from synth.cuda import gen_block_cuda
     k = gen_block_cuda(SEED, 1, DIST, layer, kv_head, 1, 0, upto, d).cpu().view(torch.int16).numpy().view(np.uint16)
@@ -535,105 +654,201 @@ def _oracle_rows(oracle, q, last, k, v, streaming, duo):
     return oracle.attention_rows(q, last, k, v)
 
 
-def cpu_baseline(hi, sample_out0, chunk_pos, dec_sample, dec_pos, L, hq, hkv, d, torch, budget_s=15.0,
-                 labels=None, duo=(0, 0), kv0=0, hkv_loc=None):
-    """Time the fp64 oracle (as it stands) on this box's host cores on a bounded sample of the same
-    workload: rows of layer 0's last timed prefill chunk; also check those rows against the GPU.
-    With duo labels (NEXT-3) the sampled streaming heads use the duo oracle."""
+class ParityAcc:
+    """max-abs / mean-abs over everything, relative L2 per (layer, q head) (reading R10)."""
+
+    def __init__(self):
+        import numpy as np
+        self.np = np
+        self.maxerr, self.sumerr, self.cnt, self.rows = 0.0, 0.0, 0, 0
+        self.sq = {}   # (layer, q head) -> [sum (o - ref)^2, sum ref^2]
+
+    def add(self, layer, qhead, got, ref):
+        np = self.np
+        err = np.abs(got - ref)
+        self.maxerr = max(self.maxerr, float(err.max()))
+        self.sumerr += float(err.sum())
+        self.cnt += err.size
+        self.rows += got.shape[0]
+        a = self.sq.setdefault((layer, qhead), [0.0, 0.0])
+        a[0] += float(((got - ref) ** 2).sum())
+        a[1] += float((ref ** 2).sum())
+
+    def result(self, prefix=""):
+        rel = {k: (v[0] ** 0.5) / max(v[1] ** 0.5, 1e-300) for k, v in self.sq.items()}
+        worst = max(rel, key=rel.get) if rel else None
+        return {f"{prefix}rows": self.rows, f"{prefix}max_abs": self.maxerr,
+                f"{prefix}mean_abs": self.sumerr / max(self.cnt, 1),
+                f"{prefix}rel_l2_max": rel[worst] if worst else None,
+                f"{prefix}rel_l2_worst_layer_qhead": list(worst) if worst else None,
+                f"{prefix}qheads_checked": len({k[1] for k in rel}),
+                f"{prefix}ok": bool(self.maxerr <= TOL_MAX_ABS and self.sumerr / max(self.cnt, 1) <= TOL_MEAN_ABS
+                                    and (not rel or rel[worst] <= TOL_REL_L2))}
+
+
+def full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, torch, labels=None, duo=(0, 0), kv0=0,
+                     hkv_loc=None, q0=0):
+    """Sampled full-size parity + the cpu baseline (SURVEY.md §8(d) "Timing procedure"), at N = 1:
+      * GPU outputs of layer 0 at the first, middle and last chunk (the last = the timed one; the first and middle
+        are re-run untimed through the same API) and of layer L-1 at the last chunk;
+      * >= 4096 (layer, q head, position) rows covering EVERY q head, the first and last row of each of those
+        chunks plus random rows, checked against the fp64 oracle (max-abs, mean-abs, rel-L2 per (layer, q head));
+      * the decode token at S (timed run) and at S + 1 (one more decode of layer 0), every q head of layer 0:
+        the full-oracle decode of one layer for 2 steps;
+      * the oracle's time on these rows gives key-visits/s on this box's cores, the baseline's tok/s on the
+        timed chunk, and an EXTRAPOLATED full 1M-prefill oracle time."""
     import numpy as np
 
     import oracle
     import synth
+    from synth.cuda import fill_
     oracle.build()
     g = hq // hkv
-    c = sample_out0.shape[0]
-    own = list(range(kv0, kv0 + (hkv if hkv_loc is None else hkv_loc)))  # global kv heads held in sample_out0
-    heads = own[:2]                    # kv heads sampled (q heads of their groups)
-    strm = {h: bool(labels is not None and labels[0][h]) for h in own}
-    if labels is not None:             # one retrieval and one streaming head when both exist
-        r_h = [h for h in own if not strm[h]][:1]
-        s_h = [h for h in own if strm[h]][:1]
-        heads = (r_h + s_h) or heads
-    kv = {h: _oracle_inputs_for_head(0, h, dec_pos + 1, d, torch) for h in heads}
-    q0 = own[0] * g                    # q heads of the owned kv heads only
-    qpre = synth.gen_block(SEED, 0, DIST, 0, q0, len(own) * g, chunk_pos, c, d)
-    # calibrate: one row per thread
+    hkv_loc = hkv if hkv_loc is None else hkv_loc
+    hq_loc = hkv_loc * g
+    own = list(range(kv0, kv0 + hkv_loc))
+    strm = {(l, h): bool(labels is not None and labels[l][h]) for l in (0, L - 1) for h in own}
     cores = oracle.num_threads()
+    # GPU: layer 0 at the first and middle chunk (untimed, same API), then decode at S + 1
+    p_mid = (S // 2) // c * c
+    chunk_out = {("last", 0): sample_outs[0], ("last", L - 1): sample_outs[L - 1]}
+    for name, pos in (("first", 0), ("mid", p_mid)):
+        if pos + c > p_last:
+            continue
+        hi.set_seq_len(0, pos)
+        Q, Kt, Vt = gen_layer_inputs(0, pos, c, hq_loc, hkv_loc, d, q0, kv0, torch, fill_)
+        chunk_out[(name, 0)] = hi.prefill_chunk(0, Q, Kt, Vt).clone()
+    hi.set_seq_len(0, S + 1)   # rows [0, S] hold the prefill and the decode token at S
+    qd1 = [fill_(torch.empty((1, n, d), dtype=torch.bfloat16, device="cuda"), SEED, t, DIST, 0, h0, S + 1)[0]
+           for t, n, h0 in ((0, hq_loc, q0), (1, hkv_loc, kv0), (2, hkv_loc, kv0))]
+    dec_next = hi.decode(0, *qd1).clone()
+    hi.synchronize()
+    chunk_pos = {"first": 0, "mid": p_mid, "last": p_last}
     rng = np.random.default_rng(0)
+    # row plan per q head: first/last row of every sampled chunk + random rows; the first chunk is cheap, so it
+    # carries most rows; >= 4096 rows in total over the sampled chunks
+    per_head = max(1, -(-4096 // hq_loc))
+    plan = {}   # (layer, name) -> token indices within the chunk
+    names = [n for n in ("first", "mid", "last") if (n, 0) in chunk_out]
+    n_last = max(2, min(24, per_head // 4))
+    n_mid = max(2, min(24, per_head // 4)) if "mid" in names else 0
+    n_first = per_head - n_last - n_mid
+    for name, n in (("first", n_first), ("mid", n_mid), ("last", n_last)):
+        if name in names:
+            plan[(0, name)] = np.unique(np.concatenate([[0, c - 1], rng.integers(1, c - 1, max(0, n - 2))]))
+    if L > 1:
+        plan[(L - 1, "last")] = np.array([0, c // 2, c - 1])
+    kvcache = {}
 
-    def rows_for(n_tok):
-        toks = np.unique(np.concatenate([[0, c - 1], rng.integers(0, c, max(0, n_tok - 2))]))[:n_tok]
-        return toks
+    def kv_of(layer, h):
+        if (layer, h) not in kvcache:
+            kvcache[(layer, h)] = _oracle_kv(layer, h, S + 2, d, torch)
+        return kvcache[(layer, h)]
 
-    # calibrate on one call of `cores` rows (the oracle parallelises over the rows of a call)
-    k0, v0 = kv[heads[0]]
-    probe_t = rows_for(cores)
-    t0 = time.time()
-    _oracle_rows(oracle, qpre[probe_t, heads[0] * g - q0], chunk_pos + probe_t, k0, v0, strm[heads[0]], duo)
-    rows_per_s = len(probe_t) / max(time.time() - t0, 1e-9)
-    n_tok = int(max(2, min(c, budget_s * rows_per_s / (g * len(heads)))))
-    toks = rows_for(n_tok)
-    t0 = time.time()
-    maxerr, sumerr, cnt, rows = 0.0, 0.0, 0, 0
-    got = sample_out0.float().cpu().numpy()
-    for h in heads:
-        k, v = kv[h]
-        for j in range(h * g, (h + 1) * g):
-            ref = _oracle_rows(oracle, qpre[toks, j - q0], chunk_pos + toks, k, v, strm[h], duo)
-            err = np.abs(got[toks, j - q0] - ref)
-            maxerr = max(maxerr, float(err.max()))
-            sumerr += float(err.sum())
-            cnt += err.size
-            rows += len(toks)
-    el = time.time() - t0
-    # decode row: the last timed decode token, sampled kv heads
-    qd = synth.gen_block(SEED, 0, DIST, 0, q0, len(own) * g, dec_pos, 1, d)[0]
-    dgot = dec_sample.float().cpu().numpy()
-    dmax = 0.0
-    for h in heads:
-        k, v = kv[h]
-        for j in range(h * g, (h + 1) * g):
-            ref = _oracle_rows(oracle, qd[j - q0:j - q0 + 1], np.array([dec_pos]), k, v, strm[h], duo)[0]
-            dmax = max(dmax, float(np.abs(dgot[j - q0] - ref).max()))
-    rows_per_tok = L * hq
-    cpu = {"value": round(rows / el / rows_per_tok, 6), "unit": "tok/s", "cores": cores, "kind": "oracle",
-           "sample": f"{rows} (layer 0, q head, position) rows of the last timed prefill chunk at positions "
-                     f"{chunk_pos}+t, q heads of kv heads {heads}, {el:.1f}s; tok/s = rows/s / "
-                     f"({L} layers x {hq} q heads)"}
-    parity = {"prefill_rows": rows, "prefill_max_abs": maxerr, "prefill_mean_abs": sumerr / max(cnt, 1),
-              "decode_rows": len(heads) * g, "decode_max_abs": dmax, "tol_max_abs": 2e-2, "tol_mean_abs": 2e-3}
-    return cpu, parity
+    acc = ParityAcc()
+    visits, t_oracle = 0.0, 0.0
+    for (layer, name), toks in plan.items():
+        pos0 = chunk_pos[name]
+        qblk = synth.gen_block(SEED, 0, DIST, layer, q0, hq_loc, pos0, c, d)
+        got = chunk_out[(name, layer)].float().cpu().numpy()
+        for h in own:
+            k, v = kv_of(layer, h)
+            js = list(range(h * g - q0, (h + 1) * g - q0))            # local q heads of kv head h
+            qrows = qblk[toks][:, js].transpose(1, 0, 2).reshape(-1, d)  # all g heads' rows in one oracle call
+            last = np.tile(pos0 + toks, g)
+            t0 = time.time()
+            ref = _oracle_rows(oracle, qrows, last, k, v, strm.get((layer, h), False), duo).reshape(g, len(toks), d)
+            t_oracle += time.time() - t0
+            visits += float((last + 1).sum())
+            for jj, jl in enumerate(js):
+                acc.add(layer, q0 + jl, got[toks, jl], ref[jj])
+        kvcache = {kk: vv for kk, vv in kvcache.items() if kk[0] == 0} if layer == L - 1 else kvcache
+    # decode: every q head of layer 0 at S (timed decode) and S + 1
+    dacc = ParityAcc()
+    t_dec = 0.0
+    for pos, out in ((S, dec_sample), (S + 1, dec_next)):
+        qd = synth.gen_block(SEED, 0, DIST, 0, q0, hq_loc, pos, 1, d)[0]
+        got = out.float().cpu().numpy()
+        for h in own:
+            k, v = kv_of(0, h)
+            t0 = time.time()
+            ref = _oracle_rows(oracle, qd[(h - kv0) * g:(h - kv0 + 1) * g], np.full(g, pos), k, v,
+                               strm.get((0, h), False), duo)
+            t_dec += time.time() - t0
+            for jj in range(g):
+                dacc.add(0, h * g + jj, got[(h - kv0) * g + jj][None], ref[jj][None])
+    parity = {**acc.result("prefill_"), **dacc.result("decode_"),
+              "chunks": {n: [chunk_pos[n], chunk_pos[n] + c] for n in names}, "layers": sorted({k[0] for k in plan}),
+              "tol_max_abs": TOL_MAX_ABS, "tol_mean_abs": TOL_MEAN_ABS, "tol_rel_l2": TOL_REL_L2}
+    parity["ok"] = parity["prefill_ok"] and parity["decode_ok"]
+    if not parity["ok"]:
+        log(f"bench: PARITY FAILURE {parity}")
+    # cpu baseline: key visits per second of the fp64 oracle on this box's cores (work per row = keys visited)
+    kv_rate = visits / max(t_oracle, 1e-9)
+    visits_timed_tok = L * hq * (p_last + (c + 1) / 2.0)        # key visits per token of the timed chunk
+    full_visits = L * hq * S * (S + 1) / 2.0                     # the whole causal prefill of S tokens
+    cpu = {"value": round(kv_rate / visits_timed_tok, 6), "unit": "tok/s", "cores": cores, "kind": "oracle",
+           "sample": f"{acc.rows} (layer, q head, position) prefill rows over every q head of layers "
+                     f"{sorted({k[0] for k in plan})}, first/last + random rows of chunks {names} "
+                     f"({t_oracle:.1f} s), + {dacc.rows} decode rows (layer 0, positions {S}, {S + 1}; {t_dec:.1f} s)",
+           "rows_per_s": round(acc.rows / max(t_oracle, 1e-9), 2), "key_visits_per_s": round(kv_rate, 1),
+           "value_definition": "key_visits_per_s / key visits per token of the timed chunk (L x Hq x (s + (c+1)/2))",
+           "decode_full_oracle_s_per_layer_token": round(t_dec / 2, 3),
+           "decode_full_oracle_s_per_token_extrapolated": round(t_dec / 2 * L, 2),
+           "extrapolated_full_prefill_oracle_s": round(full_visits / kv_rate, 1),
+           "extrapolated_note": "EXTRAPOLATED, not run: L x Hq x S(S+1)/2 key visits at the measured rate"}
+    return parity, cpu
 
 
-def sharded_parity(gathered0, chunk_pos, L, hq, hkv, d, world, torch, labels=None, duo=(0, 0), n_tok=4):
-    """Head-sharded run: rows of the all-gathered layer-0 output of the last timed chunk, one q head
-    per rank, against the oracle (checks the shard arithmetic + the collective end to end)."""
+def sharded_parity(gathered0, gdec, p_last, S, L, hq, hkv, d, world, rank, pg, torch, labels=None, duo=(0, 0),
+                   n_tok=6):
+    """Head-sharded run: rows of the all-gathered layer-0 output of the timed chunk for EVERY q head (so every
+    rank's shard and the collective are checked end to end), and the gathered decode output at S, against the
+    oracle.  The rows are split over the ranks (each rank checks the q heads of its own kv heads against the
+    GATHERED tensor, then the results are reduced)."""
     import numpy as np
 
     import oracle
     import synth
+    import torch.distributed as dist
     from paper_2502_12574_b200.parallel import to_token_major
     oracle.build()
-    full = to_token_major(gathered0).float().cpu().numpy()  # [c, hq, d]
-    c = full.shape[0]
+    c = gathered0.shape[1]
+    full = to_token_major(gathered0).float().cpu().numpy()       # [c, hq, d]
+    dfull = to_token_major(gdec).float().cpu().numpy()           # [hq, d]
     g = hq // hkv
-    toks = np.array([0, c // 3, 2 * c // 3, c - 1][:n_tok])
-    maxerr = 0.0
-    for r in range(world):
-        j = r * (hq // world)          # first q head owned by rank r
-        kv, v = _oracle_inputs_for_head(0, j // g, chunk_pos + c, d, torch)
-        q = synth.gen_block(SEED, 0, DIST, 0, j, 1, chunk_pos, c, d)[toks, 0]
-        ref = _oracle_rows(oracle, q, chunk_pos + toks, kv, v, bool(labels is not None and labels[0][j // g]), duo)
-        maxerr = max(maxerr, float(np.abs(full[toks, j] - ref).max()))
-    return {"gathered_rows": int(len(toks) * world), "max_abs": maxerr, "tol_max_abs": 2e-2}
+    toks = np.array([0, 1, c // 3, c // 2, 2 * c // 3, c - 1][:n_tok])
+    qblk = synth.gen_block(SEED, 0, DIST, 0, 0, hq, p_last, c, d)
+    qd = synth.gen_block(SEED, 0, DIST, 0, 0, hq, S, 1, d)[0]
+    acc, dacc = ParityAcc(), ParityAcc()
+    for h in range(rank * hkv // world, (rank + 1) * hkv // world):
+        k, v = _oracle_kv(0, h, S + 1, d, torch)
+        st = bool(labels is not None and labels[0][h])
+        for j in range(h * g, (h + 1) * g):
+            acc.add(0, j, full[toks, j], _oracle_rows(oracle, qblk[toks, j], p_last + toks, k, v, st, duo))
+            dacc.add(0, j, dfull[j][None], _oracle_rows(oracle, qd[j][None], np.array([S]), k, v, st, duo))
+    pr, dr = acc.result("prefill_"), dacc.result("decode_")
+    on = "cpu" if dist.get_backend(pg) == "gloo" else "cuda"
+    vals = torch.tensor([pr["prefill_max_abs"], pr["prefill_rel_l2_max"] or 0.0, dr["decode_max_abs"],
+                         dr["decode_rel_l2_max"] or 0.0, float(not (pr["prefill_ok"] and dr["decode_ok"]))],
+                        dtype=torch.float64, device=on)
+    rows = torch.tensor([pr["prefill_rows"], dr["decode_rows"]], dtype=torch.float64, device=on)
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=pg)
+    dist.all_reduce(rows, op=dist.ReduceOp.SUM, group=pg)
+    vals, rows = vals.cpu(), rows.cpu()
+    v = vals.tolist()
+    return {"gathered_prefill_rows": int(rows[0]), "qheads_checked": hq, "prefill_max_abs": v[0],
+            "prefill_rel_l2_max": v[1], "gathered_decode_rows": int(rows[1]), "decode_max_abs": v[2],
+            "decode_rel_l2_max": v[3], "ok": v[4] == 0.0, "chunk": [p_last, p_last + c], "layer": 0,
+            "tol_max_abs": TOL_MAX_ABS, "tol_rel_l2": TOL_REL_L2}
 
 
 # ---------------------------------------------------------------------------------------------
 def run_reference(args, rank, world):
     """--impl reference: the fp64 oracle (as it stands) on this box's host cores, same metric/config.
-    Each step is a bounded sample of the workload: a slice of the rows of one prefill chunk."""
+    Each step is a bounded sample of the workload: rows of the timed chunk (the last chunk before S)."""
     if rank != 0:
-        return
+        return None
     import numpy as np
     import torch
 
@@ -644,11 +859,8 @@ def run_reference(args, rank, world):
     L, hq, hkv, d, S, c = WORKLOADS[wl]
     g = hq // hkv
     pos = S - c
-    # inputs from the numpy generator for one kv head of layer 0 (bounded: first 64K keys of
-    # history are regenerated per call? no -- the whole prefix is needed; use a shorter prefix
-    # at the same shapes is NOT the workload, so take the full prefix of one head)
     if torch.cuda.is_available():
-        k, v = _oracle_inputs_for_head(0, 0, pos + c, d, torch)
+        k, v = _oracle_kv(0, 0, pos + c, d, torch)
     else:
         k = synth.gen_block(SEED, 1, DIST, 0, 0, 1, 0, pos + c, d)[:, 0]
         v = synth.gen_block(SEED, 2, DIST, 0, 0, 1, 0, pos + c, d)[:, 0]
@@ -669,20 +881,42 @@ def run_reference(args, rank, world):
         step()
     el = time.time() - t0
     val = args.steps * rows_per_step / el / (L * hq)
-    res = {"impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "tok/s", "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (same generator and workload as the ours arm)",
-           "config": {"workload": wl, "layers": L, "q_heads": hq, "kv_heads": hkv, "head_dim": d, "context": S,
-                      "chunk": c, "parallelism": "host cores"},
-           "cpu_baseline": {"value": round(val, 6), "unit": "tok/s", "cores": cores, "kind": "oracle",
-                            "sample": f"per step {rows_per_step} (layer 0, q head, position) rows of the chunk at "
-                                      f"{pos}; tok/s = rows/s / ({L} x {hq})"},
-           "e2e": {"value": round(val, 6), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(res), flush=True)
+    return {"impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (same generator and workload as the ours arm)",
+            "config": {"workload": wl, "layers": L, "q_heads": hq, "kv_heads": hkv, "head_dim": d, "context": S,
+                       "chunk": c, "timed_chunk": [pos, S], "parallelism": "host cores"},
+            "cpu_baseline": {"value": round(val, 6), "unit": "tok/s", "cores": cores, "kind": "oracle",
+                             "sample": f"per step {rows_per_step} (layer 0, q head, position) rows of the chunk at "
+                                       f"{pos}; tok/s = rows/s / ({L} x {hq})"},
+            "e2e": {"value": round(val, 6), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` (N > 1) without torchrun: re-execute this script as N ranks (one per GPU) on this node."""
+    n = args.gpus
+    if not args.ranks_share_gpu:
+        import torch
+        have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if have < n:
+            raise SystemExit(f"--gpus {n}: only {have} GPU(s) visible (use --ranks-share-gpu for a 1-GPU validation)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    log("bench: launching " + " ".join(cmd[2:]))
+    return subprocess.call(cmd, cwd=ROOT)
 
 
 def main():
+    global _JSON_FD
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -707,17 +941,29 @@ def main():
                     metavar="R/W", help="run rank R's head shard of a W-GPU job alone on this GPU (configs[3]/[4] "
                                         "on one B200: e.g. --workload 70B-1M --emulate-shard 0/8)")
     ap.add_argument("--ranks-share-gpu", action="store_true",
-                    help="validation only: every rank uses cuda:0 and the output gather goes through gloo")
+                    help="validation only: every rank uses cuda:0 and the collectives go through gloo")
     args = ap.parse_args()
     if args.warmup < 3:
         log("bench: warmup < 3 is not a valid measurement; using 3")
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(relaunch_under_torchrun(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        log(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}: running {world} ranks")
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        res = run_reference(args, rank, world)
+        if res is not None:
+            emit(res)
         return
+    # stdout carries exactly one line (rank 0's JSON): C-level stdout (NCCL's INFO log) goes to stderr
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     import torch.distributed as dist
     if args.ranks_share_gpu:
@@ -730,11 +976,16 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         pg = dist.group.WORLD
+    res = None
     try:
-        run_ours(args, rank, world, local_rank, pg)
+        res = run_ours(args, rank, world, local_rank, pg)
+        if world > 1:
+            dist.barrier(group=pg)
     finally:
         if world > 1:
             dist.destroy_process_group()
+    if res is not None:
+        emit(res)
 
 
 if __name__ == "__main__":

@@ -104,9 +104,11 @@ typedef struct hi_options {
 #define HI_FLAG_TIMING 0x8       /* bracket every attention kernel launch with timing events on the
                                     compute stream; durations are summed into hi_stats at the next
                                     hi_synchronize / hi_get_stats (bench roofline evidence) */
-#define HI_FLAG_PREFILL_2CTA 0x20     /* head_dim 128: use the CTA-pair (cta_group::2, M = 256) tcgen05 prefill
-                                         kernel instead of the single-CTA one (A/B comparisons; measured slower) */
-#define HI_FLAG_PREFILL_TC1 0x40      /* use the one-tile / three-S-buffer tcgen05 prefill kernel (k_prefill_tc1.cu) */
+/* Comparison prefill kernels (A/B measurements only; csrc/variants/).  They exist only in the variants
+ * build (build.build_variant, HI_LIB_VARIANT); the product libheadinfer.so rejects these flags with HI_EINVAL. */
+#define HI_FLAG_PREFILL_2CTA 0x20     /* head_dim 128: the CTA-pair (cta_group::2, M = 256) tcgen05 prefill kernel
+                                         instead of the single-CTA one (measured slower) */
+#define HI_FLAG_PREFILL_TC1 0x40      /* the one-tile / three-S-buffer tcgen05 prefill kernel (measured slower) */
 #define HI_FLAG_JITTER 0x80     /* hazard testing: before every history H2D block, write-back D2H and
                                    attention launch, hold that stream for a pseudo-random 0-200 us (counter hash);
                                    outputs must be bit-identical to a run without it */
@@ -114,8 +116,13 @@ typedef struct hi_options {
                                         staging block (the RAW edge of Alg. 1 l.10/13) and delay the H2D stream by
                                         2 ms per block, so attention reads slots before their bytes land; parity
                                         must FAIL (proves the tests see a missing dependency) */
-#define HI_FLAG_MMA_SYNC_PREFILL 0x10 /* run prefill attention on the legacy mma.sync kernel instead of the
-                                         tcgen05/TMEM/TMA kernel (baseline comparator for benches only) */
+#define HI_FLAG_FAULT_LAUNCH 0x200   /* FAULT INJECTION, tests only: the second hi_prefill_chunk / hi_decode call of the
+                                        context makes a kernel launch with an invalid configuration (a synchronous
+                                        CUDA error; the CUDA context survives), so the context must turn sticky */
+#define HI_FLAG_FAULT_TRAP 0x400     /* FAULT INJECTION, tests only: as above, but the injected kernel executes `trap`
+                                        (an asynchronous device fault that loses the process's CUDA context) */
+#define HI_FLAG_MMA_SYNC_PREFILL 0x10 /* variants build only: prefill attention on the legacy mma.sync kernel
+                                         instead of the tcgen05/TMEM/TMA kernel (baseline comparator) */
 
 typedef struct hi_stats {
     int64_t host_store_bytes;     /* pinned host KV bytes (L * Hkv_loc * max_ctx * 4 * d) */
@@ -223,7 +230,8 @@ int64_t hi_seq_len(const hi_ctx* ctx, int layer);
  * a chunk rewrites identical bytes).  Waits for in-flight work of the context. */
 hi_status hi_set_seq_len(hi_ctx* ctx, int layer, int64_t s);
 
-/* Snapshot of counters; waits for in-flight work of the context. */
+/* Snapshot of counters; waits for in-flight work of the context.  On a sticky-failed context the counters
+ * are still filled in (without waiting) and the call returns HI_ECUDA. */
 hi_status hi_get_stats(hi_ctx* ctx, hi_stats* out);
 
 /* Blocks until all work the context enqueued has finished. */

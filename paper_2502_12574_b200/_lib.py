@@ -25,6 +25,8 @@ HI_FLAG_PREFILL_2CTA = 0x20
 HI_FLAG_PREFILL_TC1 = 0x40
 HI_FLAG_JITTER = 0x80
 HI_FLAG_FAULT_SKIP_RAW = 0x100
+HI_FLAG_FAULT_LAUNCH = 0x200
+HI_FLAG_FAULT_TRAP = 0x400
 HI_RESIDENT_AUTO = -1
 HI_GROUP_AUTO = -1
 HI_GROUP_PAPER = -2

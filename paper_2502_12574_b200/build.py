@@ -69,12 +69,15 @@ HI_LIBS = ["-L" + CUDA_LIB, "-lcublasLt", "-Xlinker", "-rpath=" + CUDA_LIB]
 
 
 def build_variant(name: str, defines) -> str:
-    """Experiments: the same sources with extra -D flags -> build/variants/libheadinfer_<name>.so
-    (loaded when HI_LIB_VARIANT=<name>)."""
-    srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
+    """Experiments: the product sources plus the comparison prefill kernels of csrc/variants/ (mma.sync
+    baseline, CTA pair, one tile; selected by HI_FLAG_MMA_SYNC_PREFILL / _PREFILL_2CTA / _PREFILL_TC1),
+    with extra -D flags -> build/variants/libheadinfer_<name>.so (loaded when HI_LIB_VARIANT=<name>).
+    The product library (build()) does not contain the comparison kernels and rejects their flags."""
+    srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")) + glob.glob(os.path.join(PKG, "csrc", "variants", "*.cu")))
     out = os.path.join(PKG, "build", "variants", f"libheadinfer_{name}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    return _nvcc_shared(out, srcs, extra=[f"-D{d}" for d in defines], force=True, libs=HI_LIBS)
+    return _nvcc_shared(out, srcs, extra=["-DHI_WITH_VARIANTS"] + [f"-D{d}" for d in defines], force=True,
+                        libs=HI_LIBS)
 
 
 def build(force: bool = False, verbose: bool = False) -> None:

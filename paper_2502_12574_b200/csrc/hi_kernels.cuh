@@ -6,9 +6,40 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 struct hi_ctx;  // include/headinfer.h
 
 namespace hi {
+
+// Every entry point runs on the context's device and gives the caller back the current device it had
+// (one process may hold contexts on several GPUs; the caller's own device choice is not ours to change).
+struct DeviceGuard {
+    int prev = -1;
+    bool switched = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) switched = cudaSetDevice(dev) == cudaSuccess;
+        cudaGetLastError();
+    }
+    ~DeviceGuard() {
+        if (switched) cudaSetDevice(prev);
+    }
+};
+
+// Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device.  The attribute is per device,
+// so the "done" flag is kept per device ordinal (a process may hold contexts on several GPUs); setting it
+// twice from racing threads is harmless.
+template <typename K>
+cudaError_t set_smem_attr_once(K kernel, int bytes, std::atomic<unsigned long long>& done_mask) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done_mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 // Context geometry for the layer wrapper (hl_layer.cu, NEXT-4); false on NULL.
 struct CtxInfo {
@@ -111,7 +142,7 @@ struct DecodeCombineParams {
     const __nv_bfloat16* v_new;  // [Hkv_loc][d]
     const float* parts;          // [Hkv_loc][max_parts][g][d+4]
     int max_parts;
-    int16_t n_parts[MAX_LAUNCH_HEADS];  // records per local kv head (offloaded / resident / streaming differ)
+    int32_t n_parts[MAX_LAUNCH_HEADS];  // records per local kv head (offloaded / resident / streaming differ)
     int g;
     float scale_log2;
     __nv_bfloat16* out;          // [Hq_loc][d]
@@ -142,5 +173,6 @@ cudaError_t launch_duo_append(const DuoAppendParams& p, int d, cudaStream_t stre
 // ---- fill with a NaN bit pattern (poison mode, race detection) --------------------------
 cudaError_t launch_poison(void* ptr, size_t bytes, cudaStream_t stream);
 cudaError_t launch_spin(uint64_t ns, cudaStream_t stream);
+cudaError_t launch_fault(bool trap, cudaStream_t stream);
 
 }  // namespace hi

@@ -243,6 +243,7 @@ hi_status alloc_host_store(hi_ctx* c, int numa_policy, int numa_node_req) {
 
 void destroy(hi_ctx* c) {
     if (!c) return;
+    hi::DeviceGuard dg(c->device);
     if (c->s_comp) cudaStreamSynchronize(c->s_comp);
     if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
     if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
@@ -305,27 +306,32 @@ double seg_pairs(int64_t q_pos0, int n, int64_t k_pos0, int64_t n_k, bool causal
 }
 
 cudaError_t launch_prefill(hi_ctx* c, const hi::PrefillParams& p) {
+#ifdef HI_WITH_VARIANTS
+    // comparison kernels (csrc/variants/, built only into the variants library): single-head launches
     const bool mma = c->flags & HI_FLAG_MMA_SYNC_PREFILL;
     const bool pair = !mma && c->d == 128 && (c->flags & HI_FLAG_PREFILL_2CTA);
-    if (!mma && !pair && !(c->flags & HI_FLAG_PREFILL_TC1))  // the product kernel: head maps in one launch (grid.y)
-        return hi::launch_prefill_tc(p, c->d, c->s_comp);
-    for (int h = 0; h < std::max(1, p.n_heads); ++h) {  // single-head launches of the comparison kernels
-        hi::PrefillParams q1 = p;
-        q1.n_heads = 1;
-        q1.q = p.q + static_cast<int64_t>(p.head_q[h]) * p.g * c->d;
-        q1.out = p.out + static_cast<int64_t>(p.head_q[h]) * p.g * c->d;
-        q1.k = p.k + p.head_kv[h] * p.kv_head_stride;
-        q1.v = p.v + p.head_kv[h] * p.kv_head_stride;
-        q1.o_acc = p.o_acc + h * p.state_rows * c->d;
-        q1.m_acc = p.m_acc + h * p.state_rows;
-        q1.l_acc = p.l_acc + h * p.state_rows;
-        hi::set_identity_heads(q1, 1);
-        const cudaError_t e = mma ? hi::launch_prefill_mma(q1, c->d, c->s_comp)
-                              : pair ? hi::launch_prefill_tc2(q1, c->d, c->s_comp)
-                                     : hi::launch_prefill_tc1(q1, c->d, c->s_comp);
-        if (e != cudaSuccess) return e;
+    if (mma || pair || (c->flags & HI_FLAG_PREFILL_TC1)) {
+        for (int h = 0; h < std::max(1, p.n_heads); ++h) {
+            hi::PrefillParams q1 = p;
+            q1.n_heads = 1;
+            q1.q = p.q + static_cast<int64_t>(p.head_q[h]) * p.g * c->d;
+            q1.out = p.out + static_cast<int64_t>(p.head_q[h]) * p.g * c->d;
+            q1.k = p.k + p.head_kv[h] * p.kv_head_stride;
+            q1.v = p.v + p.head_kv[h] * p.kv_head_stride;
+            q1.o_acc = p.o_acc + h * p.state_rows * c->d;
+            q1.m_acc = p.m_acc + h * p.state_rows;
+            q1.l_acc = p.l_acc + h * p.state_rows;
+            hi::set_identity_heads(q1, 1);
+            const cudaError_t e = mma ? hi::launch_prefill_mma(q1, c->d, c->s_comp)
+                                  : pair ? hi::launch_prefill_tc2(q1, c->d, c->s_comp)
+                                         : hi::launch_prefill_tc1(q1, c->d, c->s_comp);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
     }
-    return cudaSuccess;
+#endif
+    // the product kernel: every head of the unit in one launch (grid.y, head maps)
+    return hi::launch_prefill_tc(p, c->d, c->s_comp);
 }
 
 hi_status check_call(hi_ctx* c, int layer) {
@@ -477,6 +483,15 @@ hi_status stage_block(hi_ctx* c, int layer, const std::vector<int>& heads, int64
     return HI_OK;
 }
 
+// HI_FLAG_FAULT_LAUNCH / HI_FLAG_FAULT_TRAP (tests): the context's second prefill/decode call injects a CUDA error
+hi_status inject_fault(hi_ctx* c) {
+    if (!(c->flags & (HI_FLAG_FAULT_LAUNCH | HI_FLAG_FAULT_TRAP)) || c->prefill_calls + c->decode_calls != 1)
+        return HI_OK;
+    HI_CK(c, hi::launch_fault(c->flags & HI_FLAG_FAULT_TRAP, c->s_comp));
+    ++c->launches;
+    return HI_OK;
+}
+
 hi_status release_slot(hi_ctx* c, int s) {
     HI_CK(c, cudaEventRecord(c->slots[s].free_, c->s_comp));
     return HI_OK;
@@ -565,6 +580,13 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
                        "head_group = -1 or >= 1 dividing kv_heads/world)";
         return HI_EINVAL;
     }
+#ifndef HI_WITH_VARIANTS
+    if (o.flags & (HI_FLAG_MMA_SYNC_PREFILL | HI_FLAG_PREFILL_2CTA | HI_FLAG_PREFILL_TC1)) {
+        g_init_error = "the comparison prefill kernels (mma.sync, CTA pair, one tile) are only in the variants "
+                       "build (paper_2502_12574_b200.build.build_variant(\"cmp\", []), HI_LIB_VARIANT=cmp)";
+        return HI_EINVAL;
+    }
+#endif
     if (kv_heads / world > hi::MAX_LAUNCH_HEADS) {
         g_init_error = "kv_heads/world must be <= 64";
         return HI_EINVAL;
@@ -617,7 +639,12 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     }
     if (opt && opt->device >= 0 && opt->device < ndev && opt->device != 0) c->device = opt->device;
     else if (cudaGetDevice(&c->device) != cudaSuccess) c->device = 0;
-    if ((e = cudaSetDevice(c->device)) != cudaSuccess) return bail(HI_ECUDA, cudaGetErrorString(e));
+    hi::DeviceGuard dg(c->device);  // the caller's current device is restored on return
+    {
+        int cur = -1;
+        if ((e = cudaGetDevice(&cur)) != cudaSuccess || cur != c->device)
+            return bail(HI_ECUDA, std::string("cannot select device ") + std::to_string(c->device));
+    }
     cudaDeviceProp prop{};
     if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess && prop.major < 10)
         return bail(HI_ECUDA, "libheadinfer is built for sm_100a (B200); device compute capability < 10");
@@ -768,6 +795,8 @@ hi_status hi_free(hi_ctx* c) {
 
 hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, const void* V, void* out, int n,
                            void* cuda_stream) {
+    if (!c) return HI_ESHAPE;
+    hi::DeviceGuard dg(c->device);
     hi_status st = check_call(c, layer);
     if (st != HI_OK) return st;
     if (!Q || !K || !V || !out) return set_err(c, HI_ESHAPE, "NULL tensor pointer");
@@ -780,6 +809,7 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
 
     HI_CK(c, cudaEventRecord(c->ev_call_in, cs));
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_call_in, 0));
+    if (hi_status fs = inject_fault(c); fs != HI_OK) return fs;
     // pack the chunk's K/V head-major (the previous call's write-back must have drained)
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_pack_free, 0));
     HI_CK(c, hi::launch_pack_kv(static_cast<const __nv_bfloat16*>(K), static_cast<const __nv_bfloat16*>(V), c->d_pack, n,
@@ -974,6 +1004,8 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
 }
 
 hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const void* v, void* out, void* cuda_stream) {
+    if (!c) return HI_ESHAPE;
+    hi::DeviceGuard dg(c->device);
     hi_status st = check_call(c, layer);
     if (st != HI_OK) return st;
     if (!q || !k || !v || !out) return set_err(c, HI_ESHAPE, "NULL tensor pointer");
@@ -986,6 +1018,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
 
     HI_CK(c, cudaEventRecord(c->ev_call_in, cs));
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_call_in, 0));
+    if (hi_status fs = inject_fault(c); fs != HI_OK) return fs;
     // copy the new k, v into this layer's kvnew buffer (its previous write-back must be done)
     __nv_bfloat16* kn = c->d_kvnew + static_cast<size_t>(layer) * 2 * Hkv * d;
     __nv_bfloat16* vn = kn + static_cast<size_t>(Hkv) * d;
@@ -997,20 +1030,21 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     // append (Alg. 1 line 26 "Async Update CPU KV cache"): host row s of every offloaded local kv head
     HI_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_packed, 0));
     if (hi_status js = jitter(c, c->s_d2h); js != HI_OK) return js;
+    // all K rows first, then all V rows: consecutive offloaded heads' rows then sit at constant source
+    // (one row) and destination (2*max_ctx rows) pitch, so each tensor is one 2-D copy per layer
     CopyBatch ap;
-    for (int h = 0; h < Hkv; ++h) {
-        if (c->streaming(layer, h)) continue;  // NEXT-3: sink / ring append below
-        if (c->resident(layer, h)) {  // H_on: append in HBM (compute stream; read by later calls only)
-            HI_CK(c, cudaMemcpyAsync(c->dev_k(layer, h, s), kn + static_cast<size_t>(h) * d, row_bytes,
-                                     cudaMemcpyDeviceToDevice, c->s_comp));
-            HI_CK(c, cudaMemcpyAsync(c->dev_v(layer, h, s), vn + static_cast<size_t>(h) * d, row_bytes,
-                                     cudaMemcpyDeviceToDevice, c->s_comp));
-            continue;
+    for (int kv = 0; kv < 2; ++kv)
+        for (int h = 0; h < Hkv; ++h) {
+            if (c->streaming(layer, h)) continue;  // NEXT-3: sink / ring append below
+            const __nv_bfloat16* src = (kv ? vn : kn) + static_cast<size_t>(h) * d;
+            if (c->resident(layer, h)) {  // H_on: append in HBM (compute stream; read by later calls only)
+                HI_CK(c, cudaMemcpyAsync(kv ? c->dev_v(layer, h, s) : c->dev_k(layer, h, s), src, row_bytes,
+                                         cudaMemcpyDeviceToDevice, c->s_comp));
+                continue;
+            }
+            ap.add(kv ? c->host_v(layer, h, s) : c->host_k(layer, h, s), src, row_bytes);
+            c->d2h_bytes += static_cast<int64_t>(row_bytes);
         }
-        ap.add(c->host_k(layer, h, s), kn + static_cast<size_t>(h) * d, row_bytes);
-        ap.add(c->host_v(layer, h, s), vn + static_cast<size_t>(h) * d, row_bytes);
-        c->d2h_bytes += static_cast<int64_t>(2 * row_bytes);
-    }
     HI_CK(c, ap.issue(c->s_d2h));
     HI_CK(c, cudaEventRecord(c->ev_kvnew_free[layer], c->s_d2h));
     HI_CK(c, cudaEventRecord(c->ev_layer_d2h[layer], c->s_d2h));
@@ -1047,7 +1081,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
         for (size_t y = 0; y < R.size(); ++y) p.kvc[y] = static_cast<int16_t>(y);
         p.kv_span = static_cast<int>(R.size());
         if ((st = launch(p, nsp, static_cast<int>(R.size()), s)) != HI_OK) return st;
-        for (int h : R) cp.n_parts[h] = static_cast<int16_t>(nsp);
+        for (int h : R) cp.n_parts[h] = static_cast<int32_t>(nsp);
     }
     const int64_t nb = (s + c->slot_tokens - 1) / c->slot_tokens;
     for (const auto& unit : c->off_units[layer]) {
@@ -1071,7 +1105,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
             st = release_slot(c, slot);
             if (st != HI_OK) return st;
         }
-        for (int h : unit) cp.n_parts[h] = static_cast<int16_t>(pofs);
+        for (int h : unit) cp.n_parts[h] = static_cast<int32_t>(pofs);
     }
     const auto& S = c->str_heads[layer];
     if (!S.empty()) {  // NEXT-3 streaming heads: the sink rows and the window's ring runs, all heads per launch
@@ -1097,7 +1131,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
             if ((st = seg(row, len)) != HI_OK) return st;
             pos += len;
         }
-        for (int h : S) cp.n_parts[h] = static_cast<int16_t>(pofs);
+        for (int h : S) cp.n_parts[h] = static_cast<int32_t>(pofs);
         // the new token's row joins the sink / ring (its ring row is not one the window above read)
         hi::DuoAppendParams ap{};
         ap.src_k = kn;
@@ -1136,6 +1170,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
 hi_status hi_synchronize(hi_ctx* c) {
     if (!c) return HI_ESHAPE;
     if (c->sticky) return HI_ECUDA;
+    hi::DeviceGuard dg(c->device);
     HI_CK(c, cudaStreamSynchronize(c->s_comp));
     HI_CK(c, cudaStreamSynchronize(c->s_h2d));
     HI_CK(c, cudaStreamSynchronize(c->s_d2h));
@@ -1144,6 +1179,8 @@ hi_status hi_synchronize(hi_ctx* c) {
 }
 
 hi_status hi_read_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, void* k_dst, void* v_dst) {
+    if (!c) return HI_ESHAPE;
+    hi::DeviceGuard dg(c->device);
     hi_status st = check_call(c, layer);
     if (st != HI_OK) return st;
     if (h < 0 || h >= c->Hkv_loc || pos < 0 || n < 0 || pos + n > c->max_ctx || (n > 0 && (!k_dst || !v_dst)))
@@ -1182,6 +1219,8 @@ hi_status hi_read_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, v
 
 hi_status hi_write_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, const void* k_src, const void* v_src,
                            int from_device) {
+    if (!c) return HI_ESHAPE;
+    hi::DeviceGuard dg(c->device);
     hi_status st = check_call(c, layer);
     if (st != HI_OK) return st;
     if (h < 0 || h >= c->Hkv_loc || pos < 0 || n < 0 || pos + n > c->max_ctx || (n > 0 && (!k_src || !v_src)))
@@ -1274,7 +1313,7 @@ hi_status hi_get_stats(hi_ctx* c, hi_stats* o) {
     o->numa_node = c->numa_node;
     o->n_slots = c->n_slots;
     o->slot_tokens = c->slot_tokens;
-    return HI_OK;
+    return c->sticky ? HI_ECUDA : HI_OK;  // a sticky-failed context still reports its counters
 }
 
 }  // extern "C"

@@ -303,7 +303,7 @@ hi_status hl_create(hi_ctx* ctx, int hidden, int inter, double rope_theta, float
         destroy(m);
         return hl_fail(nullptr, s, msg);
     };
-    if (cudaSetDevice(ci.device) != cudaSuccess) return bail(HI_ECUDA, "cudaSetDevice failed");
+    hi::DeviceGuard dg(ci.device);  // allocate on the context's device; the caller's device is restored
     const size_t c = static_cast<size_t>(ci.chunk);
     const size_t elems[8] = {c * hidden, c * (ci.Hq_loc + 2 * ci.Hkv_loc) * ci.d, c * ci.Hq_loc * ci.d,
                              c * ci.Hkv_loc * ci.d, c * ci.Hkv_loc * ci.d, c * ci.Hq_loc * ci.d,
@@ -320,12 +320,14 @@ hi_status hl_create(hi_ctx* ctx, int hidden, int inter, double rope_theta, float
 
 hi_status hl_prefill_chunk(hl_model* m, int layer_idx, const hl_weights* w, void* x, int n, void* cuda_stream) {
     if (m && (n < 1 || n > m->ci.chunk)) return hl_fail(m, HI_ESHAPE, "n_tokens must be in [1, chunk]");
+    hi::DeviceGuard dg(m ? m->ci.device : 0);
     return layer(m, layer_idx, w, x, n, static_cast<cudaStream_t>(cuda_stream), [&] {
         return hi_prefill_chunk(m->ctx, layer_idx, m->q, m->k, m->v, m->attn, n, cuda_stream);
     });
 }
 
 hi_status hl_decode(hl_model* m, int layer_idx, const hl_weights* w, void* x, void* cuda_stream) {
+    hi::DeviceGuard dg(m ? m->ci.device : 0);
     return layer(m, layer_idx, w, x, 1, static_cast<cudaStream_t>(cuda_stream), [&] {
         return hi_decode(m->ctx, layer_idx, m->q, m->k, m->v, m->attn, cuda_stream);
     });

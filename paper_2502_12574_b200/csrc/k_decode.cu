@@ -348,12 +348,8 @@ __global__ void __launch_bounds__(CB_WARPS * 32) decode_combine_kernel(const Dec
 template <int D, int G>
 cudaError_t launch_partial_dg(const DecodePartialParams& p, int n_splits, int n_heads, cudaStream_t s) {
     constexpr int smem = dm_smem_bytes<D>();
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(decode_partial_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> configured{0};
+    if (cudaError_t e = set_smem_attr_once(decode_partial_kernel<D, G>, smem, configured); e != cudaSuccess) return e;
     CUtensorMap tk, tv;
     const int64_t hs = p.kv_span > 1 ? p.kv_head_stride : static_cast<int64_t>(p.n_k) * D;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(p.n_k), static_cast<cuuint64_t>(p.kv_span)};

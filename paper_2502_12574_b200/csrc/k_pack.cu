@@ -104,4 +104,19 @@ cudaError_t launch_spin(uint64_t ns, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
+// Fault injection (HI_FLAG_FAULT_LAUNCH / HI_FLAG_FAULT_TRAP, sticky-failure tests, SURVEY.md §8(b) "a CUDA
+// error makes the ctx sticky-failed"): `trap` = a kernel that executes `trap` (asynchronous device fault, the
+// CUDA context is lost); otherwise a launch with an invalid configuration (synchronous launch error, the CUDA
+// context survives).
+__global__ void trap_kernel() { asm volatile("trap;"); }
+
+cudaError_t launch_fault(bool trap, cudaStream_t stream) {
+    if (trap) {
+        trap_kernel<<<1, 1, 0, stream>>>();
+        return cudaGetLastError();
+    }
+    spin_kernel<<<1, 4096, 0, stream>>>(0);  // 4096 threads per block: cudaErrorInvalidConfiguration
+    return cudaGetLastError();
+}
+
 }  // namespace hi

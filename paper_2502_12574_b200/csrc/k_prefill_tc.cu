@@ -901,12 +901,8 @@ cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
     const int heads = p.n_heads > 0 ? p.n_heads : 1;
     if (grid == 0) return cudaSuccess;
     if (heads > MAX_LAUNCH_HEADS || p.q_span < 1 || p.kv_span < 1) return cudaErrorInvalidValue;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(prefill_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<D>::ALLOC);
-    });
-    if (attr_err != cudaSuccess) return attr_err;
+    static std::atomic<unsigned long long> configured{0};
+    if (cudaError_t e = set_smem_attr_once(prefill_tc_kernel<D>, Smem<D>::ALLOC, configured); e != cudaSuccess) return e;
     CUtensorMap tq, tk, tv;
     {
         // (d, q heads spanned by the head map, tokens): kv head h's g rows start at coordinate h*g

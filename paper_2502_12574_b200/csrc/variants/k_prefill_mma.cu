@@ -10,7 +10,7 @@
 // fp32 accumulation, cp.async double-buffered K/V tiles, XOR-swizzled shared memory and
 // ldmatrix operand loads.  Tile: 128 query rows (GQA-packed: rows r = t*g + j) x 64 keys,
 // 8 warps x 16 rows.
-#include "hi_kernels.cuh"
+#include "../hi_kernels.cuh"
 
 #include <cuda_bf16.h>
 #include <math_constants.h>

@@ -19,8 +19,8 @@
 //
 // Warps: 0-7 softmax / O correction / epilogue; 8 TMA (Q + K ring); 9 TMEM allocator + MMA issuer;
 // 10 TMA (V ring); 11 idle.
-#include "hi_kernels.cuh"
-#include "tc_ptx.cuh"
+#include "../hi_kernels.cuh"
+#include "../tc_ptx.cuh"
 
 #include <cuda.h>
 #include <cuda_bf16.h>

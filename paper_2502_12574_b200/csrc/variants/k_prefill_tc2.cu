@@ -16,8 +16,8 @@
 // MMA commits are multicast to the barrier at the same offset in both CTAs (s_full, o_done, empty).
 // head_dim 128 only (each CTA's half of V is one 64-column SWIZZLE_128B box); d = 64 uses the
 // single-CTA kernel.
-#include "hi_kernels.cuh"
-#include "tc_ptx.cuh"
+#include "../hi_kernels.cuh"
+#include "../tc_ptx.cuh"
 
 #include <cuda.h>
 #include <cuda_bf16.h>

@@ -91,7 +91,19 @@ def test_init_rejects_invalid_options(lib, opts):
     assert b"hi_options" in lib.hi_last_error(None)
 
 
-@pytest.mark.parametrize("opts", [dict(duo_window=-5), dict(flags=0x10), dict(flags=0x20), dict(flags=0x40)])
+@pytest.mark.parametrize("flags", [0x10, 0x20, 0x40])
+def test_product_build_rejects_comparison_kernel_flags(lib, flags):
+    """The comparison prefill kernels (mma.sync, CTA pair, one tile) live only in the variants build; the
+    product library refuses their flags before touching CUDA."""
+    from paper_2502_12574_b200._lib import hi_options
+    h = ctypes.c_void_p()
+    o = hi_options(flags=flags)
+    assert lib.hi_init_ex(1, 8, 4, 64, 1024, 256, 0, 1, ctypes.byref(o), ctypes.byref(h)) == 1
+    assert not h.value
+    assert b"variants" in lib.hi_last_error(None)
+
+
+@pytest.mark.parametrize("opts", [dict(duo_window=-5), dict(duo_window=1 << 21)])
 def test_init_rejects_invalid_duo_options(lib, opts):
     """NEXT-3: streaming heads need a window >= 1 and the default (band-masking) prefill kernel."""
     from paper_2502_12574_b200._lib import hi_options

@@ -46,8 +46,17 @@ def _check_ours(res):
     assert abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-3
     ps = res["parity_sample"]
     assert ps["prefill_rows"] > 0 and ps["prefill_max_abs"] <= 2e-2 and ps["prefill_mean_abs"] <= 2e-3
-    assert ps["decode_max_abs"] <= 2e-2
+    assert ps["prefill_rel_l2_max"] <= 1e-2 and ps["decode_rel_l2_max"] <= 1e-2
+    assert ps["decode_max_abs"] <= 2e-2 and ps["ok"]
+    # every q head of the shard is checked, at the first, middle and last chunk, and 2 decode steps
+    assert ps["prefill_qheads_checked"] == res["config"]["q_heads"] // res.get("shard_emulation", {}).get("world", 1)
+    assert set(ps["chunks"]) == {"first", "mid", "last"} and ps["decode_rows"] == 2 * ps["decode_qheads_checked"]
+    cb = res["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+    assert cb["extrapolated_full_prefill_oracle_s"] > 0 and "EXTRAPOLATED" in cb["extrapolated_note"]
     assert res["e2e"]["h2d_bytes_per_step"] > 0 and res["e2e"]["d2h_bytes_per_step"] > 0
+    assert res["config"]["timed_chunk"] == [res["config"]["context"] - res["config"]["chunk"], res["config"]["context"]]
+    assert res["host_link"]["min_over_ranks"]["h2d_gbs"] > 0
 
 
 @pytest.mark.gpu
@@ -68,3 +77,27 @@ def test_bench_emulated_shard():
     assert em["rank"] == 1 and em["world"] == 2 and em["kv_heads"] == [1, 2] and em["q_heads"] == [2, 4]
     assert "rank 1 of head-shard2" in res["config"]["parallelism"]
     assert res["residency"]["host_store_bytes"] >= 1 * 1 * 2 * 1024 * 64 * 2   # 1 layer x 1 kv head (K+V)
+
+
+@pytest.mark.gpu
+def test_bench_value_independent_of_steps():
+    """Every step re-runs the same chunk, so the step time does not depend on --steps (the headline
+    drifted with --steps when the timed chunks were the last K ones)."""
+    a = run_bench("--workload", "8B-128K", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline")
+    b = run_bench("--workload", "8B-128K", "--steps", "6", "--warmup", "3", "--no-e2e", "--no-cpu-baseline")
+    assert a["config"]["timed_chunk"] == b["config"]["timed_chunk"]
+    assert abs(a["value"] / b["value"] - 1) < 0.05, (a["value"], b["value"])
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_self_launch():
+    """`--gpus 2` without torchrun re-launches itself as 2 ranks (torch.distributed.run); with one GPU the ranks
+    share cuda:0 and gather through gloo (--ranks-share-gpu).  Rank 0 prints the one JSON line: n_gpus 2, every
+    q head of the gathered output checked against the oracle."""
+    res = run_bench("--workload", "tiny", "--steps", "2", "--warmup", "3", "--gpus", "2", "--ranks-share-gpu",
+                    timeout=900)
+    assert res["n_gpus"] == 2 and res["nccl"]["comm_nranks"] == 2
+    assert "head-shard2" in res["config"]["parallelism"]
+    ps = res["parity_sample"]
+    assert ps["ok"] and ps["qheads_checked"] == 4 and ps["gathered_prefill_rows"] > 0 and ps["gathered_decode_rows"] == 4
+    assert res["value"] > 0 and res["e2e"]["value"] > 0

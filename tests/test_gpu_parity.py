@@ -163,24 +163,11 @@ def test_resident_heads_next1(resident):
     ctx.close()
 
 
-@pytest.mark.parametrize("g", [1, 4, 8])
-def test_cta_pair_kernel(g):
-    """The CTA-pair (cta_group::2, M = 256) prefill kernel behind HI_FLAG_PREFILL_2CTA (head_dim 128)."""
-    r = Run(layers=2, q_heads=2 * g, kv_heads=2, d=128, chunks=[300, 300, 555], n_decode=2, dist="P",
-            opts=dict(slot_tokens=256, flags=0x20))
-    gpu, ctx = run_gpu(r)
-    ref, inputs = run_oracle(r)
-    compare(gpu, ref)
-    check_host_kv(ctx, r, inputs)
-    ctx.close()
-
-
-@pytest.mark.parametrize("group,resident,flags", [(2, 0, 0), (4, 0, 0), (8, 0, 0), (2, 3, 0), (4, 0, 0x10),
-                                                  (2, 0, 0x20), (-1, 0, 0)])
+@pytest.mark.parametrize("group,resident,flags", [(2, 0, 0), (4, 0, 0), (8, 0, 0), (2, 3, 0), (-1, 0, 0)])
 def test_head_groups_next2(group, resident, flags):
     """NEXT-2 (§4 adaptive head-wise offloading, Tab. 5-7): `group` kv heads per H2D block and per
     kernel launch; results and host KV must not depend on the group size, with resident heads in front
-    (the groups start after them) and with the single-head kernels (mma.sync 0x10, CTA pair 0x20)."""
+    (the groups start after them)."""
     r = Run(layers=2, q_heads=16, kv_heads=8, d=128, chunks=[300, 300, 100], n_decode=4, dist="P",
             opts=dict(slot_tokens=128, head_group=group, resident_kv_heads=resident, flags=flags))
     gpu, ctx = run_gpu(r)
@@ -205,31 +192,3 @@ def test_head_groups_bit_identical_to_group1():
         outs.append(gpu[0][:589])
         ctx.close()
     assert torch.equal(outs[0], outs[1])
-
-
-@pytest.mark.parametrize("g,d", [(1, 64), (4, 64), (2, 128), (4, 128), (8, 128)])
-def test_one_tile_kernel(g, d):
-    """The one-tile / three-S-buffer prefill kernel behind HI_FLAG_PREFILL_TC1 (k_prefill_tc1.cu): causal
-    chunks, ragged tails, many history blocks, K/V multicast across CTA pairs (odd tile counts leave a
-    padding CTA)."""
-    r = Run(layers=2, q_heads=2 * g, kv_heads=2, d=d, chunks=[300, 300, 555, 77], n_decode=2, dist="P",
-            opts=dict(slot_tokens=256, flags=0x40))
-    gpu, ctx = run_gpu(r)
-    ref, inputs = run_oracle(r)
-    compare(gpu, ref)
-    check_host_kv(ctx, r, inputs)
-    ctx.close()
-
-
-@pytest.mark.parametrize("dist", ["S", "ONE"])
-def test_one_tile_kernel_special(dist):
-    """Sink-dominated scores (lazy rescale paths) and V == 1 (exact normalisation) on the one-tile kernel,
-    with head groups and resident heads."""
-    r = Run(layers=2, q_heads=16, kv_heads=4, d=128, chunks=[256, 512, 100], n_decode=2, dist=dist,
-            opts=dict(slot_tokens=192, flags=0x40, head_group=2, resident_kv_heads=1))
-    gpu, ctx = run_gpu(r)
-    if dist == "ONE":
-        assert torch.all(gpu[0] == 1.0)
-    ref, _ = run_oracle(r)
-    compare(gpu, ref)
-    ctx.close()
