@@ -793,9 +793,9 @@ def full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, t
                      f"({t_oracle:.1f} s), + {dacc.rows} decode rows (layer 0, positions {S}, {S + 1}; {t_dec:.1f} s)",
            "rows_per_s": round(acc.rows / max(t_oracle, 1e-9), 2), "key_visits_per_s": round(kv_rate, 1),
            "value_definition": "key_visits_per_s / key visits per token of the timed chunk (L x Hq x (s + (c+1)/2))",
-           "decode_full_oracle_s_per_layer_token": round(t_dec / 2, 3),
-           "decode_full_oracle_s_per_token_extrapolated": round(t_dec / 2 * L, 2),
-           "extrapolated_full_prefill_oracle_s": round(full_visits / kv_rate, 1),
+           "decode_full_oracle_s_per_layer_token": float(f"{t_dec / 2:.4g}"),
+           "decode_full_oracle_s_per_token_extrapolated": float(f"{t_dec / 2 * L:.4g}"),
+           "extrapolated_full_prefill_oracle_s": float(f"{full_visits / kv_rate:.4g}"),
            "extrapolated_note": "EXTRAPOLATED, not run: L x Hq x S(S+1)/2 key visits at the measured rate"}
     return parity, cpu
 

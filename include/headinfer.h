@@ -116,6 +116,10 @@ typedef struct hi_options {
                                         staging block (the RAW edge of Alg. 1 l.10/13) and delay the H2D stream by
                                         2 ms per block, so attention reads slots before their bytes land; parity
                                         must FAIL (proves the tests see a missing dependency) */
+#define HI_FLAG_FAULT_SKIP_BLOCK 0x800 /* NEGATIVE CONTROL, tests only: prefill skips the attention launch over the
+                                          FIRST history block of every offloaded unit (when a call has >= 2 blocks);
+                                          the parity bar (relative L2 per q head) must FAIL where the absolute bounds
+                                          alone cannot see it (near-uniform attention at long context) */
 #define HI_FLAG_FAULT_LAUNCH 0x200   /* FAULT INJECTION, tests only: the second hi_prefill_chunk / hi_decode call of the
                                         context makes a kernel launch with an invalid configuration (a synchronous
                                         CUDA error; the CUDA context survives), so the context must turn sticky */
@@ -215,7 +219,8 @@ hi_status hi_read_host_kv(hi_ctx* ctx, int layer, int kv_head_local, int64_t pos
                           void* k_dst, void* v_dst);
 
 /* Write host KV rows [pos, pos+n) of (layer, local kv head) from k_src, v_src ([n, head_dim]
- * bf16 each; device pointers if from_device != 0, else host).  Synchronous.  Does not move
+ * bf16 each; device pointers if from_device != 0, else host).  Synchronous; with a device source, all
+ * work already enqueued on the device (any stream) completes before the copy reads it.  Does not move
  * seq_len.  For a streaming head (NEXT-3) rows p < duo_sink go to its sink and rows p >= duo_sink to its
  * window ring (only the last duo_window of the range are kept).  This is the "helper for simulating or preparing decoding with large context"
  * (App. E): benches fill a long history without timing a full prefill. */

@@ -128,6 +128,17 @@ struct DecodePartialParams {
     int16_t head[MAX_LAUNCH_HEADS];
     int16_t kvc[MAX_LAUNCH_HEADS];
     int kv_span;
+    // Fused combine (the launch holds EVERY record of its heads, e.g. all-resident layers, NEXT-1): the last CTA
+    // of head y to finish (per-head completion counter, self-resetting) merges records [0, parts_total) of head
+    // head[y] with the new key by log-sum-exp and writes out rows head[y]*g .. +g; with `append` it also writes
+    // the new key/value as row n_k of kv coordinate kvc[y] (the cache row the next decode step reads).
+    int combine;
+    int append;
+    int parts_total;
+    unsigned* counters;           // [>= max head index + 1], zero between launches
+    const __nv_bfloat16* k_new;   // [*][d]: head head[y] at k_new + head[y]*d
+    const __nv_bfloat16* v_new;
+    __nv_bfloat16* out;           // [*][d]: q head head[y]*g + j
 };
 inline void set_identity_heads(DecodePartialParams& p, int n) {
     for (int i = 0; i < n && i < MAX_LAUNCH_HEADS; ++i) p.head[i] = p.kvc[i] = static_cast<int16_t>(i);

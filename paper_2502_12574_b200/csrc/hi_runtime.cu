@@ -99,6 +99,7 @@ struct hi_ctx {
     float* d_parts = nullptr;          // [Hkv_loc][max_parts][g][d+4]
     int max_parts = 0;
     __nv_bfloat16* d_kvnew = nullptr;  // [L][2][Hkv_loc][d]
+    unsigned* d_counters = nullptr;    // [Hkv_loc] fused decode combine completion counters (self-resetting)
     size_t workspace_bytes = 0;
     // NEXT-3 duo streaming heads: per (layer, kv head) a device block [K: duo_rows x d | V: duo_rows x d],
     // rows [0, duo_sink) = sink positions, rows duo_sink + (p - duo_sink) % duo_ring = the recent window
@@ -266,6 +267,7 @@ void destroy(hi_ctx* c) {
     cudaFree(c->d_lacc);
     cudaFree(c->d_parts);
     cudaFree(c->d_kvnew);
+    cudaFree(c->d_counters);
     cudaFree(c->d_res);
     cudaFree(c->d_duo);
     if (c->host) {
@@ -761,8 +763,11 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
     const size_t kvnew_b = static_cast<size_t>(layers) * 2 * c->Hkv_loc * head_dim * 2;
     if (!dmalloc(reinterpret_cast<void**>(&c->d_pack), pack_b) || !dmalloc(reinterpret_cast<void**>(&c->d_oacc), oacc_b) ||
         !dmalloc(reinterpret_cast<void**>(&c->d_macc), ml_b) || !dmalloc(reinterpret_cast<void**>(&c->d_lacc), ml_b) ||
-        !dmalloc(reinterpret_cast<void**>(&c->d_parts), parts_b) || !dmalloc(reinterpret_cast<void**>(&c->d_kvnew), kvnew_b))
+        !dmalloc(reinterpret_cast<void**>(&c->d_parts), parts_b) || !dmalloc(reinterpret_cast<void**>(&c->d_kvnew), kvnew_b) ||
+        !dmalloc(reinterpret_cast<void**>(&c->d_counters), sizeof(unsigned) * hi::MAX_LAUNCH_HEADS))
         return bail(HI_ENOMEM_DEV, "cudaMalloc of a workspace failed");
+    if (cudaMemset(c->d_counters, 0, sizeof(unsigned) * hi::MAX_LAUNCH_HEADS) != cudaSuccess)
+        return bail(HI_ECUDA, "cudaMemset of the decode counters failed");
     c->workspace_bytes = static_cast<int64_t>(pack_b + oacc_b + 2 * ml_b + parts_b + kvnew_b);
 
     auto mkev = [&](cudaEvent_t* ev) { return cudaEventCreateWithFlags(ev, cudaEventDisableTiming) == cudaSuccess; };
@@ -933,7 +938,8 @@ hi_status hi_prefill_chunk(hi_ctx* c, int layer, const void* Q, const void* K, c
             p.kv_span = static_cast<int>(unit.size());
             p.n_k = static_cast<int>(nk);
             p.k_pos0 = k0;
-            if ((st = run(p, (b == nb - 1) ? hi::PF_LAST : 0)) != HI_OK) return st;
+            const bool skip = (c->flags & HI_FLAG_FAULT_SKIP_BLOCK) && b == 0 && nb > 1;  // negative control
+            if (!skip && (st = run(p, (b == nb - 1) ? hi::PF_LAST : 0)) != HI_OK) return st;
             st = release_slot(c, slot);
             if (st != HI_OK) return st;
         }
@@ -1019,6 +1025,46 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     HI_CK(c, cudaEventRecord(c->ev_call_in, cs));
     HI_CK(c, cudaStreamWaitEvent(c->s_comp, c->ev_call_in, 0));
     if (hi_status fs = inject_fault(c); fs != HI_OK) return fs;
+    // All-resident layer (NEXT-1, Alg. 1 H_on branch l.22-23): ONE launch -- split-K over [0, s) of every kv head
+    // of the layer straight from HBM, the last CTA of each head merging its records with the new key and
+    // appending the new row in place (no kvnew staging copy, no D2H, no separate combine or append copies).
+    if (s > 0 && c->res_heads[layer].size() == static_cast<size_t>(Hkv)) {
+        const auto& R = c->res_heads[layer];
+        hi::DecodePartialParams p{};
+        p.q = static_cast<const __nv_bfloat16*>(q);
+        p.n_k = static_cast<int>(s);
+        p.split_len = decode_split_len(s, Hkv);
+        p.scale_log2 = c->scale_log2;
+        p.parts = c->d_parts;
+        p.q_head_stride = static_cast<int64_t>(g) * d;
+        p.parts_head_stride = static_cast<int64_t>(c->max_parts) * g * (d + 4);
+        for (int y = 0; y < Hkv; ++y) {
+            p.head[y] = static_cast<int16_t>(R[y]);
+            p.kvc[y] = static_cast<int16_t>(y);
+        }
+        p.kv_span = Hkv;
+        p.k = reinterpret_cast<const __nv_bfloat16*>(c->dev_k(layer, R[0], 0));
+        p.v = reinterpret_cast<const __nv_bfloat16*>(c->dev_v(layer, R[0], 0));
+        p.kv_head_stride = 2 * c->max_ctx * d;
+        const int nsp = static_cast<int>((s + p.split_len - 1) / p.split_len);
+        p.combine = 1;
+        p.append = 1;
+        p.parts_total = nsp;
+        p.counters = c->d_counters;
+        p.k_new = static_cast<const __nv_bfloat16*>(k);
+        p.v_new = static_cast<const __nv_bfloat16*>(v);
+        p.out = static_cast<__nv_bfloat16*>(out);
+        if (hi_status js = jitter(c, c->s_comp); js != HI_OK) return js;
+        LaunchTimer tm(c);
+        HI_CK(c, hi::launch_decode_partial(p, d, g, nsp, Hkv, c->s_comp));
+        tm.done(4.0 * d * static_cast<double>(s) * Hkv, T_DECODE);
+        ++c->launches;
+        st = finish_call(c, cs);
+        if (st != HI_OK) return st;
+        c->seq_len[layer] = s + 1;
+        ++c->decode_calls;
+        return HI_OK;
+    }
     // copy the new k, v into this layer's kvnew buffer (its previous write-back must be done)
     __nv_bfloat16* kn = c->d_kvnew + static_cast<size_t>(layer) * 2 * Hkv * d;
     __nv_bfloat16* vn = kn + static_cast<size_t>(Hkv) * d;
@@ -1227,6 +1273,9 @@ hi_status hi_write_host_kv(hi_ctx* c, int layer, int h, int64_t pos, int64_t n, 
         return set_err(c, HI_ESHAPE, "bad host KV range");
     st = hi_synchronize(c);
     if (st != HI_OK) return st;
+    // a device source may have been produced on any stream (e.g. the caller's): the copies below run on the
+    // library's own non-blocking streams, so everything already enqueued on the device finishes first
+    if (from_device) HI_CK(c, cudaDeviceSynchronize());
     const size_t bytes = static_cast<size_t>(n) * c->d * 2;
     if (c->streaming(layer, h)) {  // NEXT-3: sink rows, then the last duo_ring rows of the range into the ring
         const cudaMemcpyKind kind = from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;

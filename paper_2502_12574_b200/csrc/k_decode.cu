@@ -103,6 +103,63 @@ constexpr float DM_RESCALE = 8.0f;                    // lazy O rescale threshol
 template <int D>
 constexpr int dm_smem_bytes() { return DM_STAGES * 2 * (D / 64) * DM_BOX + 2 * DM_STAGES * 8 + 1024 + 1024; }
 
+// Fused combine (DecodePartialParams::combine): called by the 4 consumer warps of every CTA after its record is
+// written.  The CTA that completes head blockIdx.y's last split merges all of that head's records with the new
+// key (the token attends itself, reading R3) -- the same log-sum-exp as decode_combine_kernel -- and, with
+// `append`, stores the new key/value row for the next step.
+template <int D, int G>
+__device__ __forceinline__ void combine_tail(const DecodePartialParams& p) {
+    constexpr int NT = DM_CONSUMERS * 32;
+    __shared__ int s_last;
+    __shared__ float s_x[G];
+    const int y = blockIdx.y, h = p.head[y];
+    __threadfence();   // this CTA's record is visible device-wide before the counter says so
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[h], 1u) == gridDim.x - 1;
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    if (!s_last) return;
+    __threadfence();   // acquire: every other CTA's record of head h
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const __nv_bfloat16* qg = p.q + h * p.q_head_stride;
+    const __nv_bfloat16* kn = p.k_new + static_cast<int64_t>(h) * D;
+    const __nv_bfloat16* vn = p.v_new + static_cast<int64_t>(h) * D;
+    for (int j = warp; j < G; j += DM_CONSUMERS) {   // new key's score per q head (log2 domain)
+        float prod = 0.f;
+        for (int c = lane; c < D; c += 32) prod += __bfloat162float(qg[j * D + c]) * __bfloat162float(kn[c]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, off);
+        if (lane == 0) s_x[j] = prod * p.scale_log2;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    const float* recs = p.parts + h * p.parts_head_stride;
+    const int n = p.parts_total;
+    for (int idx = threadIdx.x; idx < G * D; idx += NT) {
+        const int j = idx / D, c = idx % D;
+        const float* rj = recs + j * (D + 4);
+        float M = s_x[j];
+        for (int i = 0; i < n; ++i) M = fmaxf(M, __ldcg(rj + static_cast<int64_t>(i) * G * (D + 4)));
+        const float a0 = fast_exp2(s_x[j] - M);
+        float L = a0, O = a0 * __bfloat162float(vn[c]);
+        for (int i = 0; i < n; ++i) {
+            const float* r = rj + static_cast<int64_t>(i) * G * (D + 4);
+            const float mi = __ldcg(r);
+            const float a = (mi == -CUDART_INF_F) ? 0.f : fast_exp2(mi - M);
+            L += a * __ldcg(r + 1);
+            O += a * __ldcg(r + 4 + c);
+        }
+        p.out[(static_cast<int64_t>(h) * G + j) * D + c] = __float2bfloat16_rn(O / L);
+    }
+    if (p.append) {   // row n_k of this head's cache: outside every range this launch read
+        __nv_bfloat16* kd = const_cast<__nv_bfloat16*>(p.k) + p.kvc[y] * p.kv_head_stride + static_cast<int64_t>(p.n_k) * D;
+        __nv_bfloat16* vd = const_cast<__nv_bfloat16*>(p.v) + p.kvc[y] * p.kv_head_stride + static_cast<int64_t>(p.n_k) * D;
+        for (int c = threadIdx.x; c < D; c += NT) {
+            kd[c] = kn[c];
+            vd[c] = vn[c];
+        }
+    }
+    if (threadIdx.x == 0) p.counters[h] = 0u;   // ready for the next launch (stream-ordered)
+}
+
 // One CTA = keys [blockIdx.x*split_len, +split_len) of the block.  A single producer thread streams
 // the CTA's K and V rows with 2-D TMA (SWIZZLE_128B boxes of 64 keys x 64 dims) into a 6-stage
 // shared-memory ring -- up to 192 KiB in flight per SM, which is what HBM latency needs.  Each of the
@@ -269,6 +326,7 @@ __global__ void __launch_bounds__(DM_THREADS, 1)
         r[4 + c] = osum;
         if (c == 0) { r[0] = mx; r[1] = lsum; }
     }
+    if (p.combine) combine_tail<D, G>(p);
 }
 
 // One CTA (8 warps) per local q head: merge the n_parts records of its kv head with the new key.

@@ -97,6 +97,16 @@ constexpr int EX2_POLY_EVERY = HI_EX2_POLY_EVERY;  // 2 of every 16 exponentials
 #define HI_POLY_PAIRS 0
 #endif
 constexpr int POLY_PAIRS = HI_POLY_PAIRS;
+// Finer choice of the polynomial pairs on the split schedule: bit k of HI_POLY_MASK8 sends element pair i
+// (i % 8 == k) to ex2_poly2 (tools/ubench/softmax_row.cu: one warp per SMSP, 3 pairs in 8 = 0x52 run a row's
+// exponentials at 3.43/cycle against 2.90 all-MUFU).  0 = all MUFU (or HI_POLY_PAIRS).
+#ifndef HI_POLY_MASK8
+#define HI_POLY_MASK8 0
+#endif
+constexpr unsigned POLY_MASK8 = HI_POLY_MASK8;
+__device__ __forceinline__ constexpr bool poly_pair(int pair) {
+    return POLY_MASK8 ? ((POLY_MASK8 >> (pair & 7)) & 1u) != 0 : (pair & 3) < POLY_PAIRS;
+}
 // Split schedule (SPLIT == 1): P(j) goes to the upper 64 S columns, so QK^T of the next KV tile's first 64
 // keys (S_lo, columns 0-63) can run as soon as the softmax has read S(j) into registers; the softmax
 // releases P in two key halves, so PV(j) over the first 64 keys overlaps the second half's
@@ -590,8 +600,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                         for (int i = LO; i < HI; i += 2) {
                             const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
-                            // POLY_PAIRS > 0 (experiment): that many of every 4 pairs on the FMA-pipe polynomial
-                            const f2 pp = ((i >> 1) & 3) < POLY_PAIRS ? ex2_poly2(a) : f2{ex2(a.x), ex2(a.y)};
+                            // POLY_PAIRS / POLY_MASK8 (experiment): some pairs on the FMA-pipe polynomial
+                            const f2 pp = poly_pair(i >> 1) ? ex2_poly2(a) : f2{ex2(a.x), ex2(a.y)};
                             acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
                             x[i / 2] = pack_bf16(pp.x, pp.y);
                         }

@@ -13,6 +13,18 @@ from synth.cuda import fill_
 
 TOL_MAX_ABS = 2e-2   # north_star: max-abs 2e-2, mean-abs 2e-3 (fp32 accumulate, bf16 out)
 TOL_MEAN_ABS = 2e-3
+# reading R10: |o| shrinks like 1/sqrt(keys) under near-uniform attention (~1e-3 at 1M), where the
+# absolute bounds cannot fail; the relative L2 error of every (layer, q head) is bounded too.  bf16 P and bf16
+# output rounding give ~2^-9 relative, so 1e-2 leaves a 3-5x margin while a dropped history block or a 2%
+# scale error fails it.
+TOL_REL_L2 = 1e-2
+
+
+def rel_l2_per_head(got: np.ndarray, ref: np.ndarray) -> np.ndarray:
+    """||got - ref|| / ||ref|| per q head over rows and dims; got/ref [rows, Hq, d]."""
+    num = np.sqrt(((got - ref) ** 2).sum(axis=(0, 2)))
+    den = np.sqrt((ref ** 2).sum(axis=(0, 2)))
+    return num / np.maximum(den, 1e-300)
 
 
 @dataclass
@@ -74,16 +86,19 @@ def run_oracle(r: Run):
     return res, inputs
 
 
-def compare(gpu_outs, ref_outs, tol_max=TOL_MAX_ABS, tol_mean=TOL_MEAN_ABS):
+def compare(gpu_outs, ref_outs, tol_max=TOL_MAX_ABS, tol_mean=TOL_MEAN_ABS, tol_rel=TOL_REL_L2):
+    """Per layer: max-abs, mean-abs and the relative L2 error of every q head (R10); all three asserted."""
     worst = {"max_abs": 0.0, "mean_abs": 0.0, "rel_l2": 0.0}
     for g, ref in zip(gpu_outs, ref_outs):
-        err = np.abs(g.double().numpy() - ref)
+        gd = g.double().numpy()
+        err = np.abs(gd - ref)
         worst["max_abs"] = max(worst["max_abs"], float(err.max()))
         worst["mean_abs"] = max(worst["mean_abs"], float(err.mean()))
-        worst["rel_l2"] = max(worst["rel_l2"], float(np.linalg.norm(g.double().numpy() - ref) / max(np.linalg.norm(ref), 1e-300)))
+        worst["rel_l2"] = max(worst["rel_l2"], float(rel_l2_per_head(gd, ref).max()))
         assert np.all(np.isfinite(g.numpy())), "non-finite GPU output"
     assert worst["max_abs"] <= tol_max, worst
     assert worst["mean_abs"] <= tol_mean, worst
+    assert worst["rel_l2"] <= tol_rel, worst
     return worst
 
 

@@ -9,6 +9,7 @@ import torch
 
 import synth
 from conftest import cuda_available
+from hi_harness import TOL_MAX_ABS, TOL_MEAN_ABS, TOL_REL_L2
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a GPU")]
 
@@ -20,6 +21,11 @@ def _gen(tensor, dist, layer, head0, nh, pos0, n, d):
     return gen_block_cuda(SEED, tensor, dist, layer, head0, nh, pos0, n, d)
 
 
+def assert_parity(e):
+    assert e["max_abs"] <= TOL_MAX_ABS and e["mean_abs"] <= TOL_MEAN_ABS, e
+    assert e["rel_l2_max"] <= TOL_REL_L2, e
+
+
 @pytest.mark.parametrize("dist,opts", [
     ("U", {}),
     ("P", {}),
@@ -27,16 +33,47 @@ def _gen(tensor, dist, layer, head0, nh, pos0, n, d):
     ("S", {"head_group": -1, "duo": 0.5}),                                     # NEXT-3 at full size
 ])
 def test_llama8b_128k_sampled_rows_and_host_kv(dist, opts):
-    _sampled_rows_and_host_kv(2, 32, 8, 128, 131072, 18944, dist, opts)
+    assert_parity(_sampled_rows_and_host_kv(2, 32, 8, 128, 131072, 18944, dist, opts))
+
+
+def test_llama8b_1m_headline_geometry_peaked():
+    """The HEADLINE geometry (bench.py's 8B-1M launch configuration): 32 q / 8 kv heads (g = 4), head group 2,
+    the default one-head staging ring (4 slots of 131072-key blocks per 2-head unit), chunk 18944 (the 1M
+    context ends in a ragged 6464-token chunk), the whole 1M context prefilled for 2 layers, under the peaked
+    distribution P (max-dominated rows: online-softmax rescaling across the 8 history blocks and the chunk
+    segment), then 3 decode steps; sampled rows of EVERY q head against the oracle (max-abs, mean-abs,
+    relative L2 per (layer, q head)) and a bit-exact scan of the whole host KV store."""
+    e = _sampled_rows_and_host_kv(2, 32, 8, 128, 1 << 20, 18944, "P", {"head_group": 2}, n_rand=16,
+                                  expect_slot_tokens=131072)
+    assert_parity(e)
 
 
 def test_llama70b_1m_rank0_of_8_sampled_rows_and_host_kv():
     """configs[4] (Llama-3-70B heads, 1M context, head-sharded over 8 GPUs) as bench.py --emulate-shard 0/8
     runs it: rank 0's kv head 0 and q heads 0-7 (g = 8), chunk 9472, the whole 1M context prefilled."""
-    _sampled_rows_and_host_kv(2, 64, 8, 128, 1 << 20, 9472, "P", {}, rank=0, world=8, n_rand=8)
+    assert_parity(_sampled_rows_and_host_kv(2, 64, 8, 128, 1 << 20, 9472, "P", {}, rank=0, world=8, n_rand=8))
 
 
-def _sampled_rows_and_host_kv(L, hq, hkv, d, S, c, dist, opts, rank=0, world=1, n_rand=24):
+def test_negative_control_scaled_output_fails_only_relative_bar():
+    """Negative control (SPEC.md S:L401 idea): the GPU rows at U/128K, scaled by 0.98, still pass the absolute
+    bounds (|o| ~ 2e-3 there) but must FAIL the relative-L2 bar -- the check the round-1 tests lacked."""
+    e = _sampled_rows_and_host_kv(1, 32, 8, 128, 131072, 18944, "U", {}, n_rand=8, scale=0.98)
+    assert e["max_abs"] <= TOL_MAX_ABS and e["mean_abs"] <= TOL_MEAN_ABS, e
+    assert e["rel_l2_max"] > TOL_REL_L2, e
+
+
+def test_negative_control_dropped_history_block_fails():
+    """Negative control: HI_FLAG_FAULT_SKIP_BLOCK drops the attention launch over the first history block of
+    every unit (a mis-merge of whole blocks).  At U/128K the absolute bounds cannot see it; the relative-L2 bar
+    must."""
+    from paper_2502_12574_b200._lib import HI_FLAG_FAULT_SKIP_BLOCK
+    e = _sampled_rows_and_host_kv(1, 32, 8, 128, 131072, 18944, "U", {"flags": HI_FLAG_FAULT_SKIP_BLOCK}, n_rand=8,
+                                  check_decode=False)
+    assert e["rel_l2_max"] > TOL_REL_L2, e
+
+
+def _sampled_rows_and_host_kv(L, hq, hkv, d, S, c, dist, opts, rank=0, world=1, n_rand=24, scale=1.0,
+                              check_decode=True, expect_slot_tokens=None):
     from oracle import attention_rows, attention_rows_duo
     from paper_2502_12574_b200.headinfer import HeadInfer
     n_dec = 3
@@ -68,7 +105,7 @@ def _sampled_rows_and_host_kv(L, hq, hkv, d, S, c, dist, opts, rank=0, world=1, 
                 o = out[torch.tensor([p - s0 for p in rows], device="cuda")].float().cpu().numpy()
                 for p, r in zip(rows, o):
                     sample.setdefault(layer, []).append((p, r))
-    for t in range(n_dec):
+    for t in range(n_dec if check_decode else 0):
         p = S + t
         for layer in range(L):
             q, k, v = (_gen(tt, dist, layer, h0, h, p, 1, d)[0] for tt, h0, h in ((0, q0, hq_loc), (1, kv0, hkv_loc),
@@ -76,10 +113,13 @@ def _sampled_rows_and_host_kv(L, hq, hkv, d, S, c, dist, opts, rank=0, world=1, 
             o = hi.decode(layer, q, k, v).float().cpu().numpy()
             sample.setdefault(layer, []).append((p, o))
     hi.synchronize()
+    if not check_decode:
+        n_dec = 0
     maxerr, sumerr, cnt = 0.0, 0.0, 0
+    rel = {}
     for layer in range(L):
         pos = np.array([p for p, _ in sample[layer]])
-        got = np.stack([r for _, r in sample[layer]])  # [R, hq_loc, d]
+        got = np.stack([r for _, r in sample[layer]]) * scale  # [R, hq_loc, d]
         qpos = np.concatenate([synth.gen_block(SEED, 0, dist, layer, q0, hq_loc, int(p), 1, d) for p in pos])
         for hl in range(hkv_loc):
             h = kv0 + hl   # global kv head
@@ -101,7 +141,13 @@ def _sampled_rows_and_host_kv(L, hq, hkv, d, S, c, dist, opts, rank=0, world=1, 
                 maxerr = max(maxerr, float(err.max()))
                 sumerr += float(err.sum())
                 cnt += err.size
+                rel[(layer, q0 + jl)] = float(np.linalg.norm(got[:, jl] - ref) / max(np.linalg.norm(ref), 1e-300))
     st = hi.stats()
     hi.close()
-    assert maxerr <= 2e-2 and sumerr / cnt <= 2e-3, (maxerr, sumerr / cnt)
     assert st["staging_bytes"] <= st["staging_bound_bytes"]
+    if expect_slot_tokens is not None:
+        assert st["slot_tokens"] == expect_slot_tokens, st
+    worst = max(rel, key=rel.get)
+    assert len({k[1] for k in rel}) == hq_loc   # every q head of the shard checked
+    return {"max_abs": maxerr, "mean_abs": sumerr / cnt, "rel_l2_max": rel[worst], "worst": worst,
+            "rows": int(cnt // d)}

@@ -37,8 +37,28 @@ def timeit(fn, reps):
     return e0.elapsed_time(e1) / reps
 
 
+def sustained(fn, seconds, flops):
+    """Back-to-back launches for `seconds` (power-capped regime, like a long prefill step), clocks sampled."""
+    from bench import ClockSampler
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        n, t = 0, 0.0
+        e0.record()
+        while t < seconds * 1e3:
+            for _ in range(20):
+                fn()
+            n += 20
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1)
+    return {"ms": round(t / n, 3), "tflops": round(flops / (t / n) / 1e9, 1), "launches": n, "clocks": clk.summary()}
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--sustain", type=float, default=0.0, help="also time cuDNN back to back for this many seconds")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--n", type=int, default=18944)
     ap.add_argument("--nk", type=int, default=131072)
@@ -64,7 +84,11 @@ def main():
         kb = k.repeat_interleave(hq // hkv, dim=1).transpose(0, 1).unsqueeze(0).contiguous()
         vb = v.repeat_interleave(hq // hkv, dim=1).transpose(0, 1).unsqueeze(0).contiguous()
         with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
-            report("torch_sdpa_cudnn", timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qb, kb, vb), a.reps))
+            fn = lambda: torch.nn.functional.scaled_dot_product_attention(qb, kb, vb)  # noqa: E731
+            report("torch_sdpa_cudnn", timeit(fn, a.reps))
+            if a.sustain > 0:
+                res["torch_sdpa_cudnn_sustained"] = sustained(fn, a.sustain, flops)
+                print("cudnn sustained", res["torch_sdpa_cudnn_sustained"], file=sys.stderr, flush=True)
         del kb, vb
     except Exception as e:  # noqa: BLE001
         res["torch_sdpa_cudnn"] = {"error": str(e)[:200]}
