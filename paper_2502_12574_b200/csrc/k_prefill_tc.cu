@@ -119,6 +119,14 @@ __device__ __forceinline__ constexpr bool poly_pair(int pair) {
 #define HI_SPLIT_S 2
 #endif
 constexpr bool SPLIT_S = HI_SPLIT_S != 0;
+// Ping-pong of the exponential phases (split schedule): the two tiles' softmax warps on one SMSP (warps q and
+// q + 4) take turns on the MUFU -- tile 0's exponentials of KV tile j, then tile 1's of j, then tile 0's of
+// j + 1 ... -- through a token mbarrier per SMSP and direction, so one tile's chain runs at the full MUFU rate
+// while the other tile's MMAs run, instead of both crawling at half rate when their phases overlap.
+#ifndef HI_PINGPONG
+#define HI_PINGPONG 0
+#endif
+constexpr bool PINGPONG = HI_PINGPONG != 0;
 constexpr bool SPLIT_S_LO = HI_SPLIT_S == 1;  // S(j+1)_lo issued early (P in the upper 64 columns)
 constexpr int P_COL = SPLIT_S_LO ? 64 : 0;    // first packed P column
 // keys whose P is released first (PV(j)_lo covers them; only PV over the rest stays on the chain)
@@ -138,8 +146,9 @@ struct __align__(8) Barriers {
     uint64_t k_full[NS], v_full[NS], kv_empty[NS];
     uint64_t s_full[2], p_full[2], o_done[2];
     uint64_t s_cons[2], p_lo[2];  // split schedule: S(j) read into registers / P(j) keys 0-63 stored
+    uint64_t tok[2][4];           // PINGPONG: MUFU token for tile t's warp on SMSP q (arrived by the other tile)
     uint32_t tmem_base;
-    uint32_t pad;
+    volatile int tile_done[2];    // PINGPONG: tile t has taken its last turn (its partner stops waiting for it)
     float xchg[2][2][BM];   // [tile][half][row]: partial row max, SPLIT=2
     float xchg_l[2][2][BM]; // [tile][half][row]: partial row sum (epilogue), SPLIT=2
 };
@@ -180,7 +189,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = p.g;
     const int n_rows = p.n_q * g;
-    const int row0 = blockIdx.x * (2 * BM);
+    // causal segment: CTA x's work grows with its rows, so the grid runs longest-first (LPT) -- the short
+    // CTAs fill the tail instead of the long ones starting last
+    const bool lpt = p.flags & PF_CAUSAL;
+    const int row0 = (lpt ? static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x)) * (2 * BM);
     const int hh = blockIdx.y;                 // kv head within the launch's head group (state index)
     const int hq = p.head_q[hh], hk = p.head_kv[hh];  // its q/out columns and k/v coordinate (head maps)
     float* const o_acc = p.o_acc + static_cast<int64_t>(hh) * p.state_rows * D;
@@ -239,7 +251,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(bar_o(t), 1);
             mbar_init(bar_sc(t), 128);
             mbar_init(bar_pl(t), 128 * SPLIT);
+            for (int q = 0; q < 4; ++q) mbar_init(smem_addr(&bars->tok[t][q]), 1);
         }
+        // a tile without KV tiles never takes a turn (its partner must not wait for it)
+        bars->tile_done[0] = n_kt0 == 0;
+        bars->tile_done[1] = n_kt1 == 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == WARP_MMA) {
@@ -693,6 +709,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tc_fence_before();
                         mbar_arrive(bar);
                     };
+                    const bool pp = PINGPONG && n_tiles == 2;
+                    if (pp && (tt == 1 || j > 0) && !bars->tile_done[tt ^ 1]) {
+                        // my turn: tile 0 before KV tile j waits for tile 1's turn j-1, tile 1 for tile 0's turn j
+                        mbar_wait(smem_addr(&bars->tok[tt][wq]), tt == 0 ? ((j - 1) & 1) : (j & 1));
+                    }
                     // keys [0, KS) -> packed columns [P_COL, P_COL + KS/2): PV(j)_lo may start
                     if (!spec_ok) exp_keys(std::integral_constant<int, 0>{}, std::integral_constant<int, KS>{});
                     tmem_st32(t_s + P_COL, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
@@ -701,6 +722,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     HI_TR(ttr + 2, j);
                     // keys [KS, 128) -> packed columns [P_COL + KS/2, P_COL + 64)
                     exp_keys(std::integral_constant<int, KS>{}, std::integral_constant<int, BN>{});
+                    if (pp) {   // pass the MUFU to the other tile's warp on this SMSP
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (j + 1 == nkt) {   // last turn: announce it BEFORE the arrive that wakes the partner
+                                bars->tile_done[tt] = 1;
+                                __threadfence_block();
+                            }
+                            mbar_arrive(smem_addr(&bars->tok[tt ^ 1][wq]));
+                        }
+                    }
                     if constexpr (KS == 64) tmem_st32(t_s + P_COL + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));
                     else tmem_st16(t_s + P_COL + 48, &x[48]);
                     release_p(bar_p(tt));
