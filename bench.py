@@ -218,9 +218,13 @@ def run_ours(args, rank, world, local_rank, pg):
         raise SystemExit(f"workload {wl}: host store {host_need / 2**30:.0f} GiB does not fit in MemAvailable "
                          f"{mem_available_bytes() / 2**30:.0f} GiB with a 24 GiB margin")
     hq_loc, hkv_loc, q0h, kv0h = sh["q_local"], sh["kv_local"], sh["q"][0], sh["kv"][0]
-    p_last = S - c                            # the timed chunk: positions [S - c, S), history S - c
+    p_last = S - c                            # the last chunk of the prefill: positions [S - c, S)
     if p_last < 0:
         raise SystemExit(f"workload {wl}: context {S} shorter than one chunk {c}")
+    # the timed chunk: its history is the token-weighted MEAN history of a chunked prefill of S tokens, (S - c)/2;
+    # a chunk's work (FLOPs s*c + c^2/2, history H2D 4d*s, write-back 4d*c) is linear in its history s, so
+    # c / t(p_t) is the whole-prefill tok/s -- the paper's metric (516 tok/s averages a whole 1M prefill)
+    p_t = p_last // 2
     max_ctx = S + 8                           # prefill to S, then decode at S (and S + 1 for parity)
     peaks = rf.load_peaks()
     shape = rf.Shape(L, hq, hkv, d)
@@ -311,11 +315,11 @@ def run_ours(args, rank, world, local_rank, pg):
                 gather_heads(outs[l], group=pg, out=gathered0 if l == 0 else gathered)
 
     # ---------------- prefill: W warm-up steps, then K timed steps, all at the last chunk [S - c, S) ------
-    step_in = make_inputs(p_last, c)
+    step_in = make_inputs(p_t, c)
     if model is not None:
         x_work = torch.empty_like(step_in)
     for i in range(W):
-        rewind(p_last)
+        rewind(p_t)
         prefill_step(step_in)
     hi.synchronize()
     st0 = hi.stats()
@@ -328,7 +332,7 @@ def run_ours(args, rank, world, local_rank, pg):
         for i in range(K):
             es = torch.cuda.Event(enable_timing=True)
             es.record(stream)
-            rewind(p_last)   # host-side cursor reset; waits for the previous step (a few us of bubble)
+            rewind(p_t)      # host-side cursor reset; waits for the previous step (a few us of bubble)
             prefill_step(step_in)
             ee = torch.cuda.Event(enable_timing=True)
             ee.record(stream)
@@ -340,7 +344,25 @@ def run_ours(args, rank, world, local_rank, pg):
     pre_ms = e0.elapsed_time(e1)
     step_ms = [a.elapsed_time(b) for a, b in step_ms]
     st1 = hi.stats()
-    sample_outs = {0: outs[0].clone(), L - 1: outs[L - 1].clone()} if model is None else {}
+    sample_outs = {("mid", 0): outs[0].clone(), ("mid", L - 1): outs[L - 1].clone()} if model is None else {}
+
+    # ---------------- the last chunk of the prefill (the most expensive one), one step, reported beside ------
+    last_in = make_inputs(p_last, c)
+    rewind(p_last)
+    torch.cuda.synchronize()
+    barrier()
+    sl0 = hi.stats()
+    e0.record(stream)
+    prefill_step(last_in)
+    hi.synchronize()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    last_ms = e0.elapsed_time(e1)
+    sl1 = hi.stats()
+    del last_in
+    if model is None:
+        sample_outs[("last", 0)] = outs[0].clone()
+        sample_outs[("last", L - 1)] = outs[L - 1].clone()
 
     # ---------------- decode: W warm-up tokens, then K timed tokens, all at context S -------------------
     dq = make_inputs(S, 1)
@@ -382,7 +404,7 @@ def run_ours(args, rank, world, local_rank, pg):
     # ---------------- e2e: the timed chunk again, inputs from pinned HOST memory --------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(hi, model, weights if model is not None else None, step_in, outs, L, c, K, W, p_last, rewind,
+        e2e = run_e2e(hi, model, weights if model is not None else None, step_in, outs, L, c, K, W, p_t, rewind,
                       world, pg, gathered, barrier, stream, torch)
     del step_in
 
@@ -397,10 +419,10 @@ def run_ours(args, rank, world, local_rank, pg):
     parity, cpu = None, None
     if not args.no_cpu_baseline and model is None:
         if world == 1:
-            parity, cpu = full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, torch,
+            parity, cpu = full_size_parity(hi, sample_outs, dec_sample, p_t, p_last, S, L, hq, hkv, d, c, torch,
                                            labels=labels, duo=duo, kv0=kv0h, hkv_loc=hkv_loc, q0=q0h)
         else:
-            parity = sharded_parity(gathered0, gdec_sample, p_last, S, L, hq, hkv, d, world, rank, pg, torch,
+            parity = sharded_parity(gathered0, gdec_sample, p_t, S, L, hq, hkv, d, world, rank, pg, torch,
                                     labels, duo)
 
     # ---------------- report (rank 0) -------------------------------------------------------------
@@ -423,7 +445,8 @@ def run_ours(args, rank, world, local_rank, pg):
     pk = dict(peaks, bf16_tflops=peak_t, **link_min)
     R = st1["resident_kv_heads"]
     dk = dict(streaming=st1["streaming_kv_heads"], n_sink=max(args.duo_sink, 0), win=args.duo_window)
-    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, p_last, c, hw, R, **dk), pk)
+    roof_p = rf.step_roofline_seconds(rf.prefill_step(shape, p_t, c, hw, R, **dk), pk)
+    roof_last = rf.step_roofline_seconds(rf.prefill_step(shape, p_last, c, hw, R, **dk), pk)
     t_roof_pre = K * roof_p["seconds"]
     roof_d = rf.step_roofline_seconds(rf.decode_step(shape, S, hw, R, **dk), pk)
     t_roof_dec = K * roof_d["seconds"]
@@ -474,12 +497,19 @@ def run_ours(args, rank, world, local_rank, pg):
                                    if args.emulate_shard is None else
                                    f"rank {hr} of head-shard{hw}, run alone on 1 GPU (no all-gather)"),
                    "prefill_step": "1 chunk x all layers (+ per-layer all-gather at N > 1)",
-                   "timed_chunk": [p_last, S], "timed_chunk_note": "every warm-up and timed step re-runs the last "
-                   "chunk of the 1M prefill (cursor rewound): value is independent of --steps",
+                   "timed_chunk": [p_t, p_t + c], "timed_chunk_note": "every warm-up and timed step re-runs the chunk "
+                   "whose history is the token-weighted mean history of the whole S-token chunked prefill, (S - c)/2 "
+                   "(cursor rewound): per-chunk work is linear in the history, so value = the whole-prefill tok/s, "
+                   "independent of --steps; the last (most expensive) chunk is in last_chunk",
                    "decode_step": "1 token x all layers", "decode_context": S,
                    "l2": "inputs per step > L2 (>= 6 GiB), no flush needed"},
         "prefill_step_ms": {"min": round(per_step[0], 3), "median": round(per_step[len(per_step) // 2], 3),
                             "max": round(per_step[-1], 3), "rank": 0},
+        "last_chunk": {"positions": [p_last, S], "tok_s": round(c / (last_ms / 1e3), 2), "ms": round(last_ms, 3),
+                       "kernel_tflops": round((sl1["prefill_attn_flops"] - sl0["prefill_attn_flops"]) /
+                                              max(sl1["prefill_attn_ms"] - sl0["prefill_attn_ms"], 1e-9) / 1e9, 1),
+                       "step_roofline_frac": round(roof_last["seconds"] / (last_ms / 1e3), 4),
+                       "note": "one step of the most expensive chunk (history S - c), rank 0, after the timed steps"},
         "decode": {"ms_per_token": round(dec_ms_tok, 3), "h2d_gbs": round(h2d_gbs, 2),
                    "link_peak_gbs": round(link_min["h2d_gbs"], 2), "link_frac": round(h2d_gbs / link_min["h2d_gbs"], 4),
                    "link_peak_source": f"measured live in this run, {world} rank(s) copying concurrently, min over ranks",
@@ -686,8 +716,8 @@ class ParityAcc:
                                     and (not rel or rel[worst] <= TOL_REL_L2))}
 
 
-def full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, torch, labels=None, duo=(0, 0), kv0=0,
-                     hkv_loc=None, q0=0):
+def full_size_parity(hi, sample_outs, dec_sample, p_t, p_last, S, L, hq, hkv, d, c, torch, labels=None, duo=(0, 0),
+                     kv0=0, hkv_loc=None, q0=0):
     """Sampled full-size parity + the cpu baseline (SURVEY.md §8(d) "Timing procedure"), at N = 1:
       * GPU outputs of layer 0 at the first, middle and last chunk (the last = the timed one; the first and middle
         are re-run untimed through the same API) and of layer L-1 at the last chunk;
@@ -709,21 +739,18 @@ def full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, t
     own = list(range(kv0, kv0 + hkv_loc))
     strm = {(l, h): bool(labels is not None and labels[l][h]) for l in (0, L - 1) for h in own}
     cores = oracle.num_threads()
-    # GPU: layer 0 at the first and middle chunk (untimed, same API), then decode at S + 1
-    p_mid = (S // 2) // c * c
-    chunk_out = {("last", 0): sample_outs[0], ("last", L - 1): sample_outs[L - 1]}
-    for name, pos in (("first", 0), ("mid", p_mid)):
-        if pos + c > p_last:
-            continue
-        hi.set_seq_len(0, pos)
-        Q, Kt, Vt = gen_layer_inputs(0, pos, c, hq_loc, hkv_loc, d, q0, kv0, torch, fill_)
-        chunk_out[(name, 0)] = hi.prefill_chunk(0, Q, Kt, Vt).clone()
+    # GPU: the timed (mean-history) chunk and the last chunk are in sample_outs; layer 0 at the first chunk is
+    # re-run untimed through the same API (it rewrites identical host rows), then one more decode at S + 1
+    chunk_out = dict(sample_outs)
+    hi.set_seq_len(0, 0)
+    Q, Kt, Vt = gen_layer_inputs(0, 0, c, hq_loc, hkv_loc, d, q0, kv0, torch, fill_)
+    chunk_out[("first", 0)] = hi.prefill_chunk(0, Q, Kt, Vt).clone()
     hi.set_seq_len(0, S + 1)   # rows [0, S] hold the prefill and the decode token at S
     qd1 = [fill_(torch.empty((1, n, d), dtype=torch.bfloat16, device="cuda"), SEED, t, DIST, 0, h0, S + 1)[0]
            for t, n, h0 in ((0, hq_loc, q0), (1, hkv_loc, kv0), (2, hkv_loc, kv0))]
     dec_next = hi.decode(0, *qd1).clone()
     hi.synchronize()
-    chunk_pos = {"first": 0, "mid": p_mid, "last": p_last}
+    chunk_pos = {"first": 0, "mid": p_t, "last": p_last}
     rng = np.random.default_rng(0)
     # row plan per q head: first/last row of every sampled chunk + random rows; the first chunk is cheap, so it
     # carries most rows; >= 4096 rows in total over the sampled chunks
@@ -738,6 +765,7 @@ def full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, t
             plan[(0, name)] = np.unique(np.concatenate([[0, c - 1], rng.integers(1, c - 1, max(0, n - 2))]))
     if L > 1:
         plan[(L - 1, "last")] = np.array([0, c // 2, c - 1])
+        plan[(L - 1, "mid")] = np.array([0, c - 1])
     kvcache = {}
 
     def kv_of(layer, h):
@@ -762,7 +790,6 @@ def full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, t
             visits += float((last + 1).sum())
             for jj, jl in enumerate(js):
                 acc.add(layer, q0 + jl, got[toks, jl], ref[jj])
-        kvcache = {kk: vv for kk, vv in kvcache.items() if kk[0] == 0} if layer == L - 1 else kvcache
     # decode: every q head of layer 0 at S (timed decode) and S + 1
     dacc = ParityAcc()
     t_dec = 0.0
@@ -785,7 +812,7 @@ def full_size_parity(hi, sample_outs, dec_sample, p_last, S, L, hq, hkv, d, c, t
         log(f"bench: PARITY FAILURE {parity}")
     # cpu baseline: key visits per second of the fp64 oracle on this box's cores (work per row = keys visited)
     kv_rate = visits / max(t_oracle, 1e-9)
-    visits_timed_tok = L * hq * (p_last + (c + 1) / 2.0)        # key visits per token of the timed chunk
+    visits_timed_tok = L * hq * (p_t + (c + 1) / 2.0)           # key visits per token of the timed chunk
     full_visits = L * hq * S * (S + 1) / 2.0                     # the whole causal prefill of S tokens
     cpu = {"value": round(kv_rate / visits_timed_tok, 6), "unit": "tok/s", "cores": cores, "kind": "oracle",
            "sample": f"{acc.rows} (layer, q head, position) prefill rows over every q head of layers "

@@ -18,7 +18,8 @@
  *   x    = x + (silu(g) * u) W_down^T              ([hidden, inter])
  *
  * Storage is bf16 at every op boundary above (reading R19 in DESIGN.md); arithmetic inside an op is
- * fp32 (GEMMs on cuBLASLt with fp32 accumulation, the norm / RoPE / SwiGLU in this library's kernels).
+ * fp32 (the projections on this library's tcgen05 GEMM with fp32 accumulation -- a streaming GEMV for a
+ * single decode token -- and the norm / RoPE / SwiGLU in its one-pass kernels).
  * Layout: every tensor is row-major, contiguous, bf16, on the context's device.  x is updated in place.
  * Head sharding is not supported here (the context's world must be 1: a tensor-parallel layer needs an
  * all-reduce after W_o and W_down that this round does not build).
@@ -61,6 +62,13 @@ hi_status hl_prefill_chunk(hl_model* m, int layer, const hl_weights* w, void* x,
 
 /* One decode token of one layer: x [hidden] in place; the attention step is hi_decode. */
 hi_status hl_decode(hl_model* m, int layer, const hl_weights* w, void* x, void* cuda_stream);
+
+/* The layer's projection as a stand-alone call (tests and benches): y[n, mo] = (beta ? y : 0) + x[n, kd] w[mo, kd]^T,
+ * row-major bf16 device tensors, fp32 accumulation, ONE rounding to bf16 (the residual add is the epilogue).
+ * n >= 2: persistent tcgen05 GEMM (128 x 256 x 64 tiles, TMA, TMEM accumulators); n == 1: streaming GEMV.
+ * mo must be a multiple of 64, kd of 8; w, x, y 16-byte aligned; ordered on cuda_stream.
+ * Errors: HI_EINVAL (sizes), HI_ECUDA. */
+hi_status hl_gemm(const void* w, const void* x, void* y, int mo, int n, int kd, int beta, void* cuda_stream);
 
 /* Release the workspaces (the hi_ctx is not freed).  NULL is a no-op. */
 hi_status hl_free(hl_model* m);

@@ -5,8 +5,8 @@
 Outputs
   paper_2502_12574_b200/libheadinfer.so   -- the C ABI (include/headinfer.h) + kernels
   synth/libsynth.so                       -- seeded input generator twin (test/bench infra)
-cudart is linked statically (nvcc default), so the libraries load on a GPU-less host too; cuBLASLt
-(NEXT-4 layer GEMMs) is linked dynamically from /usr/local/cuda/lib64 (rpath).
+cudart is linked statically (nvcc default), so the libraries load on a GPU-less host too; no other CUDA
+library is linked (the NEXT-4 layer's GEMMs are this library's own tcgen05 kernels, k_gemm.cu).
 """
 from __future__ import annotations
 
@@ -64,8 +64,7 @@ def _nvcc_shared(out: str, srcs, extra=(), force=False, verbose=False, libs=()):
     return out
 
 
-# cuBLASLt for the NEXT-4 layer's plain GEMMs (hl_layer.cu), found at run time through the rpath
-HI_LIBS = ["-L" + CUDA_LIB, "-lcublasLt", "-Xlinker", "-rpath=" + CUDA_LIB]
+HI_LIBS: list = []
 
 
 def build_variant(name: str, defines) -> str:

@@ -184,6 +184,11 @@ cudaError_t launch_duo_append(const DuoAppendParams& p, int d, cudaStream_t stre
 // ---- fill with a NaN bit pattern (poison mode, race detection) --------------------------
 cudaError_t launch_poison(void* ptr, size_t bytes, cudaStream_t stream);
 cudaError_t launch_spin(uint64_t ns, cudaStream_t stream);
+
+// ---- NEXT-4 layer projections (k_gemm.cu): y[n, mo] = (beta ? y : 0) + x[n, kd] w[mo, kd]^T, bf16 in/out, fp32
+// accumulate; tcgen05 persistent GEMM for n >= 2, an HBM-streaming GEMV for n == 1.  mo % 64 == 0, kd % 8 == 0.
+cudaError_t launch_gemm(const __nv_bfloat16* w, const __nv_bfloat16* x, __nv_bfloat16* y, int mo, int n, int kd, int beta,
+                        cudaStream_t stream);
 cudaError_t launch_fault(bool trap, cudaStream_t stream);
 
 }  // namespace hi

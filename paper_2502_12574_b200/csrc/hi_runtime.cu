@@ -285,7 +285,7 @@ void destroy(hi_ctx* c) {
 #define HI_DECODE_WAVES 3  // resident 1M decode: 1 wave 27.4 ms, 2 waves 22.6, 3 waves 21.2, 4 waves 21.4 (profiles/decode_waves_r02.txt)
 #endif
 int decode_split_len(int64_t nk, int heads = 1) {
-    const int64_t target = std::max<int64_t>(1, (HI_DECODE_WAVES * 148 + heads - 1) / heads);
+    const int64_t target = std::max<int64_t>(1, (HI_DECODE_WAVES * 148) / heads);   // never a partial extra wave
     int64_t s = (nk + target - 1) / target;
     s = (s + 63) / 64 * 64;
     return static_cast<int>(std::max<int64_t>(64, std::min<int64_t>(s, 1 << 30)));

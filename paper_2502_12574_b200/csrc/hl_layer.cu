@@ -3,21 +3,20 @@
 //
 // Per call, on the caller's stream:
 //   rmsnorm_kernel      xn = bf16(x * rsqrt(mean(x^2) + eps) * gamma)          (fp32 inside)
-//   cuBLASLt GEMM       qkv = bf16(xn W_qkv^T)                                 (fp32 accumulate)
+//   gemm (k_gemm.cu)    qkv = bf16(xn W_qkv^T)                                 (tcgen05, fp32 accumulate)
 //   rope_split_kernel   Q, K = bf16(rope(q, k)), V = v, split head-major for the attention call
 //   hi_prefill_chunk / hi_decode   a = attention(Q, K, V)                      (the offloaded path)
-//   cuBLASLt GEMM       x = bf16(x + a W_o^T)          (beta = 1, D aliases C: the residual is the epilogue)
+//   gemm                x = bf16(x + a W_o^T)          (beta = 1: the residual is the epilogue)
 //   rmsnorm_kernel      xn = ... mlp_norm
-//   cuBLASLt GEMM       gu = bf16(xn W_gate_up^T)
+//   gemm                gu = bf16(xn W_gate_up^T)
 //   swiglu_kernel       act = bf16(silu(g) * u)
-//   cuBLASLt GEMM       x = bf16(x + act W_down^T)
-// The GEMMs are plain library GEMMs (cuBLASLt); the elementwise / normalisation steps are HBM-bound
-// one-pass kernels with 16-byte accesses.  RoPE angles are reduced in fp64 (p * inv_freq reaches 1e6 rad
+//   gemm                x = bf16(x + act W_down^T)
+// The projections run on this library's tcgen05 GEMM (k_gemm.cu; a streaming GEMV for one decode token); the
+// elementwise / normalisation steps are HBM-bound one-pass kernels with 16-byte accesses.  RoPE angles are reduced in fp64 (p * inv_freq reaches 1e6 rad
 // at 1M context, where an fp32 product would already be off by ~0.06 rad), then sin/cos in fp32.
 #include "../../include/hilayer.h"
 #include "hi_kernels.cuh"
 
-#include <cublasLt.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -151,10 +150,6 @@ struct hl_model {
     float eps = 0.f;
     double inv_freq[MAX_HALF_D] = {0};
     std::string err = "no error";
-    cublasLtHandle_t lt = nullptr;
-    void* lt_ws = nullptr;
-    size_t lt_ws_bytes = size_t(32) << 20;
-    std::map<std::tuple<int, int, int, int>, cublasLtMatmulAlgo_t> algos;
     __nv_bfloat16 *xn = nullptr, *qkv = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr,
                   *gu = nullptr, *act = nullptr;
     int64_t launches = 0;
@@ -174,47 +169,12 @@ hi_status ck(hl_model* m, cudaError_t e, const char* what) {
     return hl_fail(m, HI_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// Y[n, mo] (+)= X[n, k] W[mo, k]^T, all row-major bf16; beta 0 or 1 (1: Y holds the residual, D aliases C).
+// Y[n, mo] (+)= X[n, k] W[mo, k]^T, all row-major bf16; beta 0 or 1 (1: Y holds the residual, the sum is rounded
+// once in the epilogue).  k_gemm.cu: tcgen05 GEMM (n >= 2) or GEMV (n == 1, decode).
 hi_status gemm(hl_model* m, const __nv_bfloat16* W, const __nv_bfloat16* X, __nv_bfloat16* Y, int mo, int n, int kd,
                float beta, cudaStream_t st) {
-    cublasLtMatmulDesc_t op = nullptr;
-    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-    cublasStatus_t s = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F);
-    const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
-    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof tA);
-    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof tB);
-    // column-major view: A = W^T stored [kd x mo] (ld kd), op T -> mo x kd; B = X^T [kd x n]; C = Y^T [mo x n]
-    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatrixLayoutCreate(&la, CUDA_R_16BF, kd, mo, kd);
-    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatrixLayoutCreate(&lb, CUDA_R_16BF, kd, n, kd);
-    if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatrixLayoutCreate(&lc, CUDA_R_16BF, mo, n, mo);
-    const auto key = std::make_tuple(mo, n, kd, beta != 0.f ? 1 : 0);
-    auto it = m->algos.find(key);
-    if (s == CUBLAS_STATUS_SUCCESS && it == m->algos.end()) {
-        cublasLtMatmulPreference_t pref = nullptr;
-        s = cublasLtMatmulPreferenceCreate(&pref);
-        if (s == CUBLAS_STATUS_SUCCESS)
-            s = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &m->lt_ws_bytes,
-                                                     sizeof m->lt_ws_bytes);
-        cublasLtMatmulHeuristicResult_t res{};
-        int found = 0;
-        if (s == CUBLAS_STATUS_SUCCESS) s = cublasLtMatmulAlgoGetHeuristic(m->lt, op, la, lb, lc, lc, pref, 1, &res, &found);
-        if (pref) cublasLtMatmulPreferenceDestroy(pref);
-        if (s == CUBLAS_STATUS_SUCCESS && found == 0) s = CUBLAS_STATUS_NOT_SUPPORTED;
-        if (s == CUBLAS_STATUS_SUCCESS) it = m->algos.emplace(key, res.algo).first;
-    }
-    const float alpha = 1.f;
-    if (s == CUBLAS_STATUS_SUCCESS)
-        s = cublasLtMatmul(m->lt, op, &alpha, W, la, X, lb, &beta, Y, lc, Y, lc, &it->second, m->lt_ws, m->lt_ws_bytes, st);
-    if (lc) cublasLtMatrixLayoutDestroy(lc);
-    if (lb) cublasLtMatrixLayoutDestroy(lb);
-    if (la) cublasLtMatrixLayoutDestroy(la);
-    if (op) cublasLtMatmulDescDestroy(op);
-    if (s != CUBLAS_STATUS_SUCCESS) {
-        char buf[128];
-        snprintf(buf, sizeof buf, "cuBLASLt matmul %dx%dx%d failed (status %d)", mo, n, kd, static_cast<int>(s));
-        return hl_fail(m, HI_ECUDA, buf);
-    }
-    return HI_OK;
+    ++m->launches;
+    return ck(m, hi::launch_gemm(W, X, Y, mo, n, kd, beta != 0.f ? 1 : 0, st), "launch_gemm");
 }
 
 hi_status rmsnorm(hl_model* m, const __nv_bfloat16* x, const void* gamma, __nv_bfloat16* out, int n, cudaStream_t st) {
@@ -271,8 +231,6 @@ void destroy(hl_model* m) {
     if (!m) return;
     cudaDeviceSynchronize();
     for (__nv_bfloat16* p : {m->xn, m->qkv, m->q, m->k, m->v, m->attn, m->gu, m->act}) cudaFree(p);
-    cudaFree(m->lt_ws);
-    if (m->lt) cublasLtDestroy(m->lt);
     cudaGetLastError();
     delete m;
 }
@@ -312,8 +270,6 @@ hi_status hl_create(hi_ctx* ctx, int hidden, int inter, double rope_theta, float
     for (int i = 0; i < 8; ++i)
         if (cudaMalloc(reinterpret_cast<void**>(bufs[i]), elems[i] * 2) != cudaSuccess)
             return bail(HI_ENOMEM_DEV, "cudaMalloc of a layer workspace failed");
-    if (cudaMalloc(&m->lt_ws, m->lt_ws_bytes) != cudaSuccess) return bail(HI_ENOMEM_DEV, "cuBLASLt workspace");
-    if (cublasLtCreate(&m->lt) != CUBLAS_STATUS_SUCCESS) return bail(HI_ECUDA, "cublasLtCreate failed");
     *out = m;
     return HI_OK;
 }
@@ -331,6 +287,19 @@ hi_status hl_decode(hl_model* m, int layer_idx, const hl_weights* w, void* x, vo
     return layer(m, layer_idx, w, x, 1, static_cast<cudaStream_t>(cuda_stream), [&] {
         return hi_decode(m->ctx, layer_idx, m->q, m->k, m->v, m->attn, cuda_stream);
     });
+}
+
+hi_status hl_gemm(const void* w, const void* x, void* y, int mo, int n, int kd, int beta, void* cuda_stream) {
+    if (!w || !x || !y || mo <= 0 || n <= 0 || kd <= 0 || mo % 64 || kd % 8)
+        return hl_fail(nullptr, HI_EINVAL, "hl_gemm: NULL pointer or sizes (mo % 64, kd % 8)");
+    const cudaError_t e = hi::launch_gemm(static_cast<const __nv_bfloat16*>(w), static_cast<const __nv_bfloat16*>(x),
+                                          static_cast<__nv_bfloat16*>(y), mo, n, kd, beta ? 1 : 0,
+                                          static_cast<cudaStream_t>(cuda_stream));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return hl_fail(nullptr, HI_ECUDA, std::string("hl_gemm: ") + cudaGetErrorString(e));
+    }
+    return HI_OK;
 }
 
 hi_status hl_free(hl_model* m) {

@@ -65,3 +65,19 @@ class HeadInferLayer:
             self.close()
         except Exception:
             pass
+
+
+def hl_gemm(w: torch.Tensor, x: torch.Tensor, y: torch.Tensor, beta: bool = False,
+            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """include/hilayer.h hl_gemm: y[n, mo] = (beta ? y : 0) + x[n, kd] w[mo, kd]^T (bf16, fp32 accumulate, one
+    rounding).  Argument marshalling only."""
+    mo, kd = w.shape
+    n = x.shape[0]
+    for t, shp, name in ((w, (mo, kd), "w"), (x, (n, kd), "x"), (y, (n, mo), "y")):
+        if not t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous() or tuple(t.shape) != shp:
+            raise ValueError(f"{name} must be a contiguous CUDA bf16 tensor of shape {shp}")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    st = _lib.load().hl_gemm(w.data_ptr(), x.data_ptr(), y.data_ptr(), mo, n, kd, 1 if beta else 0, s.cuda_stream)
+    if st != _lib.HI_OK:
+        raise _lib.HIError(st, _lib.load().hl_last_error(None).decode(errors="replace"))
+    return y
