@@ -345,6 +345,7 @@ def run_ours(args, rank, world, local_rank, pg):
     step_ms = [a.elapsed_time(b) for a, b in step_ms]
     st1 = hi.stats()
     sample_outs = {("mid", 0): outs[0].clone(), ("mid", L - 1): outs[L - 1].clone()} if model is None else {}
+    gathered_mid = gathered0.clone() if gathered0 is not None else None   # the last-chunk step below re-gathers
 
     # ---------------- the last chunk of the prefill (the most expensive one), one step, reported beside ------
     last_in = make_inputs(p_last, c)
@@ -405,7 +406,7 @@ def run_ours(args, rank, world, local_rank, pg):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(hi, model, weights if model is not None else None, step_in, outs, L, c, K, W, p_t, rewind,
-                      world, pg, gathered, barrier, stream, torch)
+                      world, pg, gathered, barrier, stream, torch, ref_outs=sample_outs)
     del step_in
 
     # ---------------- max over ranks --------------------------------------------------------------
@@ -422,7 +423,7 @@ def run_ours(args, rank, world, local_rank, pg):
             parity, cpu = full_size_parity(hi, sample_outs, dec_sample, p_t, p_last, S, L, hq, hkv, d, c, torch,
                                            labels=labels, duo=duo, kv0=kv0h, hkv_loc=hkv_loc, q0=q0h)
         else:
-            parity = sharded_parity(gathered0, gdec_sample, p_t, S, L, hq, hkv, d, world, rank, pg, torch,
+            parity = sharded_parity(gathered_mid, gdec_sample, p_t, S, L, hq, hkv, d, world, rank, pg, torch,
                                     labels, duo)
 
     # ---------------- report (rank 0) -------------------------------------------------------------
@@ -548,6 +549,7 @@ def run_ours(args, rank, world, local_rank, pg):
     if e2e:
         res["e2e"] = {"value": round(K * c / (e2e_ms / 1e3), 2), "unit": "tok/s",
                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                      "bit_identical_to_resident_run": e2e.get("bit_identical_to_resident_run"),
                       "overlap": "layer l+1's Q/K/V H2D on a side stream under layer l's attention; out D2H on "
                                  "another side stream"}
     if parity is not None:
@@ -581,7 +583,8 @@ def run_ours(args, rank, world, local_rank, pg):
     return res
 
 
-def run_e2e(hi, model, weights, step_in, outs, L, c, K, W, p_last, rewind, world, pg, gathered, barrier, stream, torch):
+def run_e2e(hi, model, weights, step_in, outs, L, c, K, W, p_last, rewind, world, pg, gathered, barrier, stream, torch,
+            ref_outs=None):
     """The timed chunk through the public API from pinned HOST buffers: per step, every layer's Q/K/V go host ->
     device (double-buffered, layer l+1's copy on a side stream under layer l's attention) and every layer's `out`
     device -> host (side stream); both inside the timed region."""
@@ -660,7 +663,7 @@ def run_e2e(hi, model, weights, step_in, outs, L, c, K, W, p_last, rewind, world
         if i >= W:
             e2e_ms += e0.elapsed_time(e1)
     # the e2e outputs are the same chunk as the timed one: they must equal the resident-input outputs bit for bit
-    same = all(torch.equal(host_out[l], outs[l].cpu()) for l in (0, L - 1))
+    same = all(torch.equal(host_out[l], ref_outs[("mid", l)].cpu()) for l in (0, L - 1))
     if not same:
         log("bench: WARNING e2e outputs differ from the resident-input run")
     return {"ms": e2e_ms, "h2d": h2d_b, "d2h": d2h_b, "bit_identical_to_resident_run": same}

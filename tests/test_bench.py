@@ -55,7 +55,10 @@ def _check_ours(res):
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
     assert cb["extrapolated_full_prefill_oracle_s"] > 0 and "EXTRAPOLATED" in cb["extrapolated_note"]
     assert res["e2e"]["h2d_bytes_per_step"] > 0 and res["e2e"]["d2h_bytes_per_step"] > 0
-    assert res["config"]["timed_chunk"] == [res["config"]["context"] - res["config"]["chunk"], res["config"]["context"]]
+    S, c = res["config"]["context"], res["config"]["chunk"]
+    assert res["config"]["timed_chunk"] == [(S - c) // 2, (S - c) // 2 + c]   # the mean-history chunk
+    assert res["last_chunk"]["positions"] == [S - c, S] and res["last_chunk"]["tok_s"] > 0
+    assert res["e2e"]["bit_identical_to_resident_run"]
     assert res["host_link"]["min_over_ranks"]["h2d_gbs"] > 0
 
 
