@@ -272,9 +272,29 @@ def run_ours(args, rank, world, local_rank, pg):
 
     stream = torch.cuda.current_stream()
 
+    wk = torch.empty((max(args.duo_window, 1), 1, d), dtype=torch.bfloat16, device="cuda") if labels is not None else None
+    wv = torch.empty_like(wk) if wk is not None else None
+
+    def refill_windows(pos, layers=None):
+        """Duo streaming heads (NEXT-3) keep only their sink rows and a ring of the last `win` rows: a cursor moved
+        back to `pos` must get the window below `pos` back (the same generator bytes a prefill wrote there)."""
+        ns, win = max(args.duo_sink, 0), args.duo_window
+        for l in (range(L) if layers is None else layers):
+            for h in range(hkv_loc):
+                if not labels[l][kv0h + h]:
+                    continue
+                lo = max(ns, pos - win)
+                if pos > lo:
+                    n = pos - lo
+                    fill_(wk[:n], SEED, 1, DIST, l, kv0h + h, lo)
+                    fill_(wv[:n], SEED, 2, DIST, l, kv0h + h, lo)
+                    hi.write_host_kv(l, h, lo, wk[:n, 0], wv[:n, 0])
+
     def rewind(pos):
         for l in range(L):
             hi.set_seq_len(l, pos)
+        if labels is not None:
+            refill_windows(pos)
 
     # ---------------- the step: attention path only (default), or whole synthetic layers (--model, NEXT-4)
     model = None
@@ -328,21 +348,19 @@ def run_ours(args, rank, world, local_rank, pg):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ms = []
     with ClockSampler(local_rank) as clk_p:
-        e0.record(stream)
         for i in range(K):
+            rewind(p_t)      # cursor reset (+ duo windows put back): between the timed steps, not in them
             es = torch.cuda.Event(enable_timing=True)
             es.record(stream)
-            rewind(p_t)      # host-side cursor reset; waits for the previous step (a few us of bubble)
             prefill_step(step_in)
+            hi.synchronize()  # the step ends when its last write-back has drained
             ee = torch.cuda.Event(enable_timing=True)
             ee.record(stream)
             step_ms.append((es, ee))
-        hi.synchronize()  # drain the write-back stream too
-        e1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    pre_ms = e0.elapsed_time(e1)
     step_ms = [a.elapsed_time(b) for a, b in step_ms]
+    pre_ms = sum(step_ms)
     st1 = hi.stats()
     sample_outs = {("mid", 0): outs[0].clone(), ("mid", L - 1): outs[L - 1].clone()} if model is None else {}
     gathered_mid = gathered0.clone() if gathered0 is not None else None   # the last-chunk step below re-gathers
@@ -371,7 +389,6 @@ def run_ours(args, rank, world, local_rank, pg):
     gdec = torch.empty((world, hq_loc, d), dtype=torch.bfloat16, device="cuda") if world > 1 else None
 
     def decode_step():
-        rewind(S)
         if model is not None:
             xd = dq[0].clone()
             for l in range(L):
@@ -384,20 +401,23 @@ def run_ours(args, rank, world, local_rank, pg):
                 gather_heads(dout[l], group=pg, out=gdec)
 
     for i in range(W):
+        rewind(S)
         decode_step()
     hi.synchronize()
     sd0 = hi.stats()
     torch.cuda.synchronize()
     barrier()
+    dec_ms = 0.0
     with ClockSampler(local_rank) as clk_d:
-        e0.record(stream)
         for i in range(K):
+            rewind(S)
+            e0.record(stream)
             decode_step()
-        hi.synchronize()
-        e1.record(stream)
-        torch.cuda.synchronize()
+            hi.synchronize()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dec_ms += e0.elapsed_time(e1)
     barrier()
-    dec_ms = e0.elapsed_time(e1)
     sd1 = hi.stats()
     dec_sample = dout[0].clone() if model is None else None
     gdec_sample = gdec.clone() if gdec is not None else None
@@ -421,7 +441,8 @@ def run_ours(args, rank, world, local_rank, pg):
     if not args.no_cpu_baseline and model is None:
         if world == 1:
             parity, cpu = full_size_parity(hi, sample_outs, dec_sample, p_t, p_last, S, L, hq, hkv, d, c, torch,
-                                           labels=labels, duo=duo, kv0=kv0h, hkv_loc=hkv_loc, q0=q0h)
+                                           labels=labels, duo=duo, kv0=kv0h, hkv_loc=hkv_loc, q0=q0h,
+                                           restore=(lambda pos: refill_windows(pos, [0])) if labels is not None else None)
         else:
             parity = sharded_parity(gathered_mid, gdec_sample, p_t, S, L, hq, hkv, d, world, rank, pg, torch,
                                     labels, duo)
@@ -720,7 +741,7 @@ class ParityAcc:
 
 
 def full_size_parity(hi, sample_outs, dec_sample, p_t, p_last, S, L, hq, hkv, d, c, torch, labels=None, duo=(0, 0),
-                     kv0=0, hkv_loc=None, q0=0):
+                     kv0=0, hkv_loc=None, q0=0, restore=None):
     """Sampled full-size parity + the cpu baseline (SURVEY.md §8(d) "Timing procedure"), at N = 1:
       * GPU outputs of layer 0 at the first, middle and last chunk (the last = the timed one; the first and middle
         are re-run untimed through the same API) and of layer L-1 at the last chunk;
@@ -749,6 +770,8 @@ def full_size_parity(hi, sample_outs, dec_sample, p_t, p_last, S, L, hq, hkv, d,
     Q, Kt, Vt = gen_layer_inputs(0, 0, c, hq_loc, hkv_loc, d, q0, kv0, torch, fill_)
     chunk_out[("first", 0)] = hi.prefill_chunk(0, Q, Kt, Vt).clone()
     hi.set_seq_len(0, S + 1)   # rows [0, S] hold the prefill and the decode token at S
+    if restore is not None:    # duo streaming heads: their window below S + 1 (the e2e leg re-ran an earlier chunk)
+        restore(S + 1)
     qd1 = [fill_(torch.empty((1, n, d), dtype=torch.bfloat16, device="cuda"), SEED, t, DIST, 0, h0, S + 1)[0]
            for t, n, h0 in ((0, hq_loc, q0), (1, hkv_loc, kv0), (2, hkv_loc, kv0))]
     dec_next = hi.decode(0, *qd1).clone()
@@ -983,8 +1006,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and "WORLD_SIZE" in os.environ:
         log(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}: running {world} ranks")
-    if args.impl == "reference":
-        res = run_reference(args, rank, world)
+    if args.impl == "reference":   # rank 0 alone runs the oracle (the other ranks of a torchrun launch exit 0)
+        res = run_reference(args, rank, max(world, args.gpus))
         if res is not None:
             emit(res)
         return
