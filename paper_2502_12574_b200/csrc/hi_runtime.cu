@@ -284,8 +284,11 @@ void destroy(hi_ctx* c) {
 #ifndef HI_DECODE_WAVES
 #define HI_DECODE_WAVES 3  // resident 1M decode: 1 wave 27.4 ms, 2 waves 22.6, 3 waves 21.2, 4 waves 21.4 (profiles/decode_waves_r02.txt)
 #endif
-int decode_split_len(int64_t nk, int heads = 1) {
-    const int64_t target = std::max<int64_t>(1, (HI_DECODE_WAVES * 148) / heads);   // never a partial extra wave
+// Offloaded history blocks are decoded while the NEXT block crosses the host link (~100x slower than HBM), so
+// their launches need no more than one wave: fewer, longer CTAs amortise the ring's fill and the launch ramp.
+constexpr int kOffloadDecodeWaves = 1;
+int decode_split_len(int64_t nk, int heads = 1, int waves = HI_DECODE_WAVES) {
+    const int64_t target = std::max<int64_t>(1, (waves * 148) / heads);   // never a partial extra wave
     int64_t s = (nk + target - 1) / target;
     s = (s + 63) / 64 * 64;
     return static_cast<int>(std::max<int64_t>(64, std::min<int64_t>(s, 1 << 30)));
@@ -1101,10 +1104,11 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
     // history -> split-K partial records, per local kv head h at parts[h][0 .. n_parts[h])
     hi::DecodeCombineParams cp{};
     const int64_t rec = static_cast<int64_t>(g) * (d + 4);
-    auto partial = [&](hi::DecodePartialParams& p, const std::vector<int>& heads, int64_t nk, int pofs) -> int {
+    auto partial = [&](hi::DecodePartialParams& p, const std::vector<int>& heads, int64_t nk, int pofs,
+                       int waves = HI_DECODE_WAVES) -> int {
         p.q = static_cast<const __nv_bfloat16*>(q);
         p.n_k = static_cast<int>(nk);
-        p.split_len = decode_split_len(nk, static_cast<int>(heads.size()));
+        p.split_len = decode_split_len(nk, static_cast<int>(heads.size()), waves);
         p.scale_log2 = c->scale_log2;
         p.parts = c->d_parts + pofs * rec;
         p.q_head_stride = static_cast<int64_t>(g) * d;
@@ -1143,7 +1147,7 @@ hi_status hi_decode(hi_ctx* c, int layer, const void* q, const void* k, const vo
             st = stage_block(c, layer, unit, k0, nk, &slot);
             if (st != HI_OK) return st;
             hi::DecodePartialParams p{};
-            const int nsp = partial(p, unit, nk, pofs);
+            const int nsp = partial(p, unit, nk, pofs, kOffloadDecodeWaves);
             p.k = reinterpret_cast<const __nv_bfloat16*>(c->slot_k(slot));
             p.v = reinterpret_cast<const __nv_bfloat16*>(c->slot_v(slot));
             p.kv_head_stride = static_cast<int64_t>(c->slot_head_bytes() / 2);
