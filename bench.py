@@ -302,12 +302,25 @@ def run_ours(args, rank, world, local_rank, pg):
     if args.model:
         from paper_2502_12574_b200.layer import HeadInferLayer
         from synth.cuda import fill_matrix_, gen_layer_weights_cuda
-        if world != 1:
-            raise SystemExit("--model runs at world 1 (the layer wrapper has no tensor parallelism)")
+        from paper_2502_12574_b200.layer import shard_layer_weights
+        from paper_2502_12574_b200.parallel import tp_layer_step
         H, I = MODEL_DIMS
         model = HeadInferLayer(hi, H, I, MODEL_ROPE_THETA, MODEL_RMS_EPS)
-        weights = [gen_layer_weights_cuda(SEED, l, H, I, hq, hkv, d) for l in range(L)]
+        weights = []
+        for l in range(L):   # full weights per layer, then this rank's tensor-parallel shard (world > 1)
+            wl = gen_layer_weights_cuda(SEED, l, H, I, hq, hkv, d)
+            weights.append(wl if hw == 1 else shard_layer_weights(wl, hq, hkv, d, I, hr, hw))
+            del wl
         torch.cuda.synchronize()
+        tp_bufs = {"y": torch.empty((c, H), dtype=torch.float32, device="cuda"),
+                   "z": torch.empty((c, H), dtype=torch.float32, device="cuda")} if world > 1 else None
+
+    def model_layer(l, x, decode=False):
+        if world == 1:
+            return model.decode(l, weights[l], x) if decode else model.prefill_chunk(l, weights[l], x)
+        n = 1 if decode else x.shape[0]
+        return tp_layer_step(model, l, weights[l], x, group=pg, decode=decode,
+                             bufs={k: v[:n] for k, v in tp_bufs.items()})
 
     def make_inputs(pos, n):
         """One step's inputs: per-layer (Q, K, V) for the attention path; x [n, H] for --model."""
@@ -326,7 +339,7 @@ def run_ours(args, rank, world, local_rank, pg):
         if model is not None:   # x flows through every layer in place: start every step from the same x
             x_work.copy_(inputs)
             for l in range(L):
-                model.prefill_chunk(l, weights[l], x_work)
+                model_layer(l, x_work)
             return
         for l in range(L):
             Q, Kt, Vt = inputs[l]
@@ -392,7 +405,7 @@ def run_ours(args, rank, world, local_rank, pg):
         if model is not None:
             xd = dq[0].clone()
             for l in range(L):
-                model.decode(l, weights[l], xd)
+                model_layer(l, xd, decode=True)
             return
         for l in range(L):
             q, k, v = dq[l]
@@ -425,7 +438,7 @@ def run_ours(args, rank, world, local_rank, pg):
     # ---------------- e2e: the timed chunk again, inputs from pinned HOST memory --------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(hi, model, weights if model is not None else None, step_in, outs, L, c, K, W, p_t, rewind,
+        e2e = run_e2e(hi, model_layer if model is not None else None, None, step_in, outs, L, c, K, W, p_t, rewind,
                       world, pg, gathered, barrier, stream, torch, ref_outs=sample_outs)
     del step_in
 
@@ -580,8 +593,9 @@ def run_ours(args, rank, world, local_rank, pg):
     if model is not None:
         H, I = MODEL_DIMS
         gemm_tok = L * 2.0 * (H * (hq + 2 * hkv) * d + H * hq * d + 3 * H * I)  # QKV, O, gate+up, down
-        t_gemm = K * c * gemm_tok / (peak_t * 1e12)
-        res["config"]["path"] = "synthetic Llama-3-8B decoder layers (NEXT-4): RMSNorm, QKV/O/MLP GEMMs, RoPE, SwiGLU"
+        t_gemm = K * c * gemm_tok / hw / (peak_t * 1e12)   # each rank runs 1/W of the projections (tensor parallel)
+        res["config"]["path"] = ("synthetic Llama-3-8B decoder layers (NEXT-4): RMSNorm, QKV/O/MLP GEMMs, RoPE, SwiGLU"
+                                 + (f"; tensor parallel over {world} ranks (2 all-reduces per layer)" if world > 1 else ""))
         res["data"] = ("synthetic (seeded counter-hash generator): hidden states in, random-init Llama-3-8B layer "
                        "weights (no trained weights, no embedding / LM head)")
         res["config"]["hidden"], res["config"]["intermediate"] = H, I
@@ -623,7 +637,7 @@ def run_e2e(hi, model, weights, step_in, outs, L, c, K, W, p_last, rewind, world
             e0.record(stream)
             dev_x.copy_(host_x, non_blocking=True)
             for l in range(L):
-                model.prefill_chunk(l, weights[l], dev_x)
+                model(l, dev_x)   # model_layer: the single-rank layer, or the tensor-parallel one
             host_out.copy_(dev_x, non_blocking=True)
             hi.synchronize()
             e1.record(stream)

@@ -21,8 +21,19 @@
  * fp32 (the projections on this library's tcgen05 GEMM with fp32 accumulation -- a streaming GEMV for a
  * single decode token -- and the norm / RoPE / SwiGLU in its one-pass kernels).
  * Layout: every tensor is row-major, contiguous, bf16, on the context's device.  x is updated in place.
- * Head sharding is not supported here (the context's world must be 1: a tensor-parallel layer needs an
- * all-reduce after W_o and W_down that this round does not build).
+ *
+ * Tensor parallelism (a context created with world W > 1, SURVEY.md §8(f) NEXT-4 "70B via TP"): the layer
+ * splits like the attention path -- rank r owns the q / kv heads of its head shard and the intermediate
+ * columns [r*inter/W, (r+1)*inter/W).  Its weights are the matching shards: w_qkv = the rank's q-head rows, then
+ * its k-head rows, then its v-head rows ([(Hq_loc + 2 Hkv_loc) d, hidden]); w_o = the rank's q-head columns
+ * ([hidden, Hq_loc d]); w_gate_up = the rank's gate rows then its up rows ([2 inter/W, hidden]); w_down = the
+ * rank's intermediate columns ([hidden, inter/W]); the norms are replicated.  x is replicated.  A layer is then
+ *   hl_attn_partial   -> y  (fp32 [n, hidden]: this rank's a W_o^T, unrounded)      caller: all-reduce(y, sum)
+ *   hl_mlp_partial    -> x = bf16(x + y); z (fp32: this rank's act W_down^T)        caller: all-reduce(z, sum)
+ *   hl_residual_add   -> x = bf16(x + z)
+ * which is the single-rank layer with the two residual sums rounded once each, up to the fp32 order of the sum
+ * over ranks (at W = 1 the three calls are bit-identical to hl_prefill_chunk / hl_decode).  The collectives are
+ * the caller's (NCCL through torch.distributed); hl_prefill_chunk / hl_decode need world == 1 (HI_ESTATE otherwise).
  *
  * Ownership: the caller owns x and the weights; the model owns its workspaces (sized for the context's
  * chunk) and never retains caller pointers.  All work is ordered on the caller's stream.
@@ -50,9 +61,9 @@ typedef struct hl_weights {
 } hl_weights;
 
 /*
- * hl_create -- workspaces (for up to the context's `chunk` tokens) and a cuBLASLt handle for layers
- * around `ctx`'s attention.  hidden, inter: multiples of 64; rope_theta > 0; rms_eps > 0.
- * Errors: HI_EINVAL (sizes, world != 1), HI_ENOMEM_DEV, HI_ECUDA.
+ * hl_create -- workspaces (for up to the context's `chunk` tokens) for layers around `ctx`'s attention.
+ * hidden: multiple of 64; inter: multiple of 64 * world; rope_theta > 0; rms_eps > 0.
+ * Errors: HI_EINVAL (sizes), HI_ENOMEM_DEV, HI_ECUDA.
  */
 hi_status hl_create(hi_ctx* ctx, int hidden, int inter, double rope_theta, float rms_eps, hl_model** out);
 
@@ -62,6 +73,14 @@ hi_status hl_prefill_chunk(hl_model* m, int layer, const hl_weights* w, void* x,
 
 /* One decode token of one layer: x [hidden] in place; the attention step is hi_decode. */
 hi_status hl_decode(hl_model* m, int layer, const hl_weights* w, void* x, void* cuda_stream);
+
+/* Tensor-parallel halves of one layer (see above).  decode != 0: one token (n must be 1), attention = hi_decode.
+ * y_f32 / z_f32: fp32 [n, hidden] device buffers the call writes.  Errors as hl_prefill_chunk. */
+hi_status hl_attn_partial(hl_model* m, int layer, const hl_weights* w, const void* x, int n, int decode, void* y_f32,
+                          void* cuda_stream);
+hi_status hl_mlp_partial(hl_model* m, int layer, const hl_weights* w, void* x, const void* y_f32, int n, void* z_f32,
+                         void* cuda_stream);
+hi_status hl_residual_add(hl_model* m, void* x, const void* z_f32, int n, void* cuda_stream);
 
 /* The layer's projection as a stand-alone call (tests and benches): y[n, mo] = (beta ? y : 0) + x[n, kd] w[mo, kd]^T,
  * row-major bf16 device tensors, fp32 accumulation, ONE rounding to bf16 (the residual add is the epilogue).

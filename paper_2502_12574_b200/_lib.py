@@ -36,7 +36,8 @@ HI_GROUP_PAPER = -2
 EXPORTS = ["hi_init", "hi_init_ex", "hi_prefill_chunk", "hi_decode", "hi_free", "hi_read_host_kv",
            "hi_write_host_kv", "hi_seq_len", "hi_set_seq_len", "hi_get_stats", "hi_synchronize",
            "hi_status_str", "hi_last_error",
-           "hl_create", "hl_prefill_chunk", "hl_decode", "hl_free", "hl_last_error", "hl_gemm"]
+           "hl_create", "hl_prefill_chunk", "hl_decode", "hl_free", "hl_last_error", "hl_gemm",
+           "hl_attn_partial", "hl_mlp_partial", "hl_residual_add"]
 
 
 class hi_options(ctypes.Structure):
@@ -107,6 +108,11 @@ def load() -> ctypes.CDLL:
     lib.hl_free.argtypes = [P]
     lib.hl_gemm.argtypes = [VP, VP, VP, I, I, I, I, VP]
     lib.hl_gemm.restype = I
+    lib.hl_attn_partial.argtypes = [P, I, ctypes.POINTER(hl_weights), VP, I, I, VP, VP]
+    lib.hl_mlp_partial.argtypes = [P, I, ctypes.POINTER(hl_weights), VP, VP, I, VP, VP]
+    lib.hl_residual_add.argtypes = [P, VP, VP, I, VP]
+    for name in ["hl_attn_partial", "hl_mlp_partial", "hl_residual_add"]:
+        getattr(lib, name).restype = I
     lib.hl_last_error.argtypes = [P]
     lib.hl_last_error.restype = ctypes.c_char_p
     for name in ["hl_create", "hl_prefill_chunk", "hl_decode", "hl_free"]:

@@ -95,6 +95,8 @@ struct PrefillParams {
     // i > p - win for query position p (the recent window).  The runtime only passes win > 0 for segments
     // that hold no sink keys (k_pos0 >= n_sink); sink segments are plain (all visible).
     int win;
+    int row_rev;              // set by the launcher: CTA x takes the rows of CTA |row_rev - x| (grid - 1 for causal
+                              // segments: longest-first); 0 = in order
 };
 inline void set_identity_heads(PrefillParams& p, int n) {
     for (int i = 0; i < n && i < MAX_LAUNCH_HEADS; ++i) p.head_q[i] = p.head_kv[i] = static_cast<int16_t>(i);
@@ -187,8 +189,9 @@ cudaError_t launch_spin(uint64_t ns, cudaStream_t stream);
 
 // ---- NEXT-4 layer projections (k_gemm.cu): y[n, mo] = (beta ? y : 0) + x[n, kd] w[mo, kd]^T, bf16 in/out, fp32
 // accumulate; tcgen05 persistent GEMM for n >= 2, an HBM-streaming GEMV for n == 1.  mo % 64 == 0, kd % 8 == 0.
-cudaError_t launch_gemm(const __nv_bfloat16* w, const __nv_bfloat16* x, __nv_bfloat16* y, int mo, int n, int kd, int beta,
-                        cudaStream_t stream);
+// out_f32: y is fp32 and written unrounded (beta must be 0) -- the tensor-parallel layer's partial sums.
+cudaError_t launch_gemm(const __nv_bfloat16* w, const __nv_bfloat16* x, void* y, int mo, int n, int kd, int beta,
+                        int out_f32, cudaStream_t stream);
 cudaError_t launch_fault(bool trap, cudaStream_t stream);
 
 }  // namespace hi

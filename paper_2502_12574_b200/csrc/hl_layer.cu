@@ -141,12 +141,27 @@ __global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat1
     }
 }
 
+// x[i] = bf16(x[i] + y[i]): the residual add of a tensor-parallel layer after its fp32 partial sums were
+// all-reduced (one rounding, as the fused GEMM epilogue of the single-rank layer)
+__global__ void residual_add_kernel(__nv_bfloat16* __restrict__ x, const float* __restrict__ y, int64_t n8) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint4 u = reinterpret_cast<uint4*>(x)[i];
+        const float4 a = reinterpret_cast<const float4*>(y)[2 * i], b = reinterpret_cast<const float4*>(y)[2 * i + 1];
+        __nv_bfloat16* e = reinterpret_cast<__nv_bfloat16*>(&u);
+        const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = __float2bfloat16_rn(bf(e[j]) + f[j]);
+        reinterpret_cast<uint4*>(x)[i] = u;
+    }
+}
+
 }  // namespace
 
 struct hl_model {
     hi_ctx* ctx = nullptr;
     hi::CtxInfo ci{};
-    int H = 0, I = 0;
+    int H = 0, I = 0;   // I = this rank's intermediate columns (inter / world)
     float eps = 0.f;
     double inv_freq[MAX_HALF_D] = {0};
     std::string err = "no error";
@@ -171,10 +186,18 @@ hi_status ck(hl_model* m, cudaError_t e, const char* what) {
 
 // Y[n, mo] (+)= X[n, k] W[mo, k]^T, all row-major bf16; beta 0 or 1 (1: Y holds the residual, the sum is rounded
 // once in the epilogue).  k_gemm.cu: tcgen05 GEMM (n >= 2) or GEMV (n == 1, decode).
-hi_status gemm(hl_model* m, const __nv_bfloat16* W, const __nv_bfloat16* X, __nv_bfloat16* Y, int mo, int n, int kd,
-               float beta, cudaStream_t st) {
+hi_status gemm(hl_model* m, const __nv_bfloat16* W, const __nv_bfloat16* X, void* Y, int mo, int n, int kd,
+               float beta, cudaStream_t st, bool out_f32 = false) {
     ++m->launches;
-    return ck(m, hi::launch_gemm(W, X, Y, mo, n, kd, beta != 0.f ? 1 : 0, st), "launch_gemm");
+    return ck(m, hi::launch_gemm(W, X, Y, mo, n, kd, beta != 0.f ? 1 : 0, out_f32 ? 1 : 0, st), "launch_gemm");
+}
+
+hi_status residual_add(hl_model* m, __nv_bfloat16* x, const float* y, int n, cudaStream_t st) {
+    const int64_t n8 = static_cast<int64_t>(n) * m->H / 8;
+    const int grid = static_cast<int>(std::min<int64_t>((n8 + 255) / 256, 148 * 8));
+    residual_add_kernel<<<grid, 256, 0, st>>>(x, y, n8);
+    ++m->launches;
+    return ck(m, cudaGetLastError(), "residual_add_kernel");
 }
 
 hi_status rmsnorm(hl_model* m, const __nv_bfloat16* x, const void* gamma, __nv_bfloat16* out, int n, cudaStream_t st) {
@@ -183,15 +206,21 @@ hi_status rmsnorm(hl_model* m, const __nv_bfloat16* x, const void* gamma, __nv_b
     return ck(m, cudaGetLastError(), "rmsnorm_kernel");
 }
 
-// Everything of the layer except the attention call; `attend` runs hi_prefill_chunk / hi_decode.
-template <typename Attend>
-hi_status layer(hl_model* m, int layer_idx, const hl_weights* w, void* xv, int n, cudaStream_t st, Attend attend) {
+hi_status check_layer(hl_model* m, int layer_idx, const hl_weights* w, const void* xv) {
     if (!m) return HI_ESHAPE;
     if (!w || !xv || !w->attn_norm || !w->w_qkv || !w->w_o || !w->mlp_norm || !w->w_gate_up || !w->w_down)
         return hl_fail(m, HI_ESHAPE, "NULL weight or activation pointer");
     if (layer_idx < 0 || layer_idx >= m->ci.L) return hl_fail(m, HI_ESHAPE, "layer out of range");
+    return HI_OK;
+}
+
+// Attention half of the layer: xn = rmsnorm(x), this rank's q|k|v = xn W_qkv^T, RoPE, the offloaded attention
+// (`attend`: hi_prefill_chunk / hi_decode), then the O projection: x = bf16(x + a W_o^T) in the GEMM epilogue
+// (y == NULL, single rank), or the fp32 partial y = a W_o^T of this rank's heads (tensor parallel).
+template <typename Attend>
+hi_status attn_half(hl_model* m, int layer_idx, const hl_weights* w, __nv_bfloat16* x, int n, float* y, cudaStream_t st,
+                    Attend attend) {
     const int64_t s = hi_seq_len(m->ctx, layer_idx);
-    __nv_bfloat16* x = static_cast<__nv_bfloat16*>(xv);
     const int hq = m->ci.Hq_loc, hkv = m->ci.Hkv_loc, d = m->ci.d;
     hi_status r;
     if ((r = rmsnorm(m, x, w->attn_norm, m->xn, n, st)) != HI_OK) return r;
@@ -215,7 +244,14 @@ hi_status layer(hl_model* m, int layer_idx, const hl_weights* w, void* xv, int n
         m->err = std::string("attention: ") + hi_last_error(m->ctx);
         return r;
     }
-    if ((r = gemm(m, static_cast<const __nv_bfloat16*>(w->w_o), m->attn, x, m->H, n, hq * d, 1.f, st)) != HI_OK) return r;
+    if (y) return gemm(m, static_cast<const __nv_bfloat16*>(w->w_o), m->attn, y, m->H, n, hq * d, 0.f, st, true);
+    return gemm(m, static_cast<const __nv_bfloat16*>(w->w_o), m->attn, x, m->H, n, hq * d, 1.f, st);
+}
+
+// MLP half: xn = rmsnorm(x), this rank's gate|up = xn W_gate_up^T, SwiGLU, down projection: x = bf16(x + act W_down^T)
+// (z == NULL, single rank) or the fp32 partial z = act W_down^T of this rank's intermediate columns.
+hi_status mlp_half(hl_model* m, const hl_weights* w, __nv_bfloat16* x, int n, float* z, cudaStream_t st) {
+    hi_status r;
     if ((r = rmsnorm(m, x, w->mlp_norm, m->xn, n, st)) != HI_OK) return r;
     if ((r = gemm(m, static_cast<const __nv_bfloat16*>(w->w_gate_up), m->xn, m->gu, 2 * m->I, n, m->H, 0.f, st)) != HI_OK)
         return r;
@@ -224,7 +260,20 @@ hi_status layer(hl_model* m, int layer_idx, const hl_weights* w, void* xv, int n
     swiglu_kernel<<<grid, 256, 0, st>>>(m->gu, m->act, n, m->I);
     ++m->launches;
     if ((r = ck(m, cudaGetLastError(), "swiglu_kernel")) != HI_OK) return r;
+    if (z) return gemm(m, static_cast<const __nv_bfloat16*>(w->w_down), m->act, z, m->H, n, m->I, 0.f, st, true);
     return gemm(m, static_cast<const __nv_bfloat16*>(w->w_down), m->act, x, m->H, n, m->I, 1.f, st);
+}
+
+// The whole single-rank layer; `attend` runs hi_prefill_chunk / hi_decode.
+template <typename Attend>
+hi_status layer(hl_model* m, int layer_idx, const hl_weights* w, void* xv, int n, cudaStream_t st, Attend attend) {
+    hi_status r = check_layer(m, layer_idx, w, xv);
+    if (r != HI_OK) return r;
+    if (m->ci.world != 1)
+        return hl_fail(m, HI_ESTATE, "head-sharded context: use hl_attn_partial / hl_mlp_partial / hl_residual_add");
+    __nv_bfloat16* x = static_cast<__nv_bfloat16*>(xv);
+    if ((r = attn_half(m, layer_idx, w, x, n, nullptr, st, attend)) != HI_OK) return r;
+    return mlp_half(m, w, x, n, nullptr, st);
 }
 
 void destroy(hl_model* m) {
@@ -246,14 +295,14 @@ hi_status hl_create(hi_ctx* ctx, int hidden, int inter, double rope_theta, float
     *out = nullptr;
     hi::CtxInfo ci{};
     if (!hi::ctx_info(ctx, &ci)) return hl_fail(nullptr, HI_EINVAL, "ctx is NULL");
-    if (hidden <= 0 || inter <= 0 || hidden % 64 || inter % 64 || !(rope_theta > 0.0) || !(rms_eps > 0.f))
-        return hl_fail(nullptr, HI_EINVAL, "hidden and inter must be positive multiples of 64; rope_theta, rms_eps > 0");
-    if (ci.world != 1) return hl_fail(nullptr, HI_EINVAL, "the layer wrapper needs world == 1 (no tensor parallelism)");
+    if (hidden <= 0 || inter <= 0 || hidden % 64 || inter % (64 * ci.world) || !(rope_theta > 0.0) || !(rms_eps > 0.f))
+        return hl_fail(nullptr, HI_EINVAL, "hidden must be a positive multiple of 64, inter of 64 * world; "
+                                           "rope_theta, rms_eps > 0");
     hl_model* m = new hl_model();
     m->ctx = ctx;
     m->ci = ci;
     m->H = hidden;
-    m->I = inter;
+    m->I = inter / ci.world;   // tensor parallel: this rank's intermediate columns
     m->eps = rms_eps;
     for (int i = 0; i < ci.d / 2; ++i) m->inv_freq[i] = pow(rope_theta, -2.0 * i / ci.d);
     auto bail = [&](hi_status s, const char* msg) {
@@ -265,7 +314,7 @@ hi_status hl_create(hi_ctx* ctx, int hidden, int inter, double rope_theta, float
     const size_t c = static_cast<size_t>(ci.chunk);
     const size_t elems[8] = {c * hidden, c * (ci.Hq_loc + 2 * ci.Hkv_loc) * ci.d, c * ci.Hq_loc * ci.d,
                              c * ci.Hkv_loc * ci.d, c * ci.Hkv_loc * ci.d, c * ci.Hq_loc * ci.d,
-                             c * 2 * inter, c * inter};
+                             c * 2 * static_cast<size_t>(m->I), c * static_cast<size_t>(m->I)};
     __nv_bfloat16** bufs[8] = {&m->xn, &m->qkv, &m->q, &m->k, &m->v, &m->attn, &m->gu, &m->act};
     for (int i = 0; i < 8; ++i)
         if (cudaMalloc(reinterpret_cast<void**>(bufs[i]), elems[i] * 2) != cudaSuccess)
@@ -289,12 +338,46 @@ hi_status hl_decode(hl_model* m, int layer_idx, const hl_weights* w, void* x, vo
     });
 }
 
+hi_status hl_attn_partial(hl_model* m, int layer_idx, const hl_weights* w, const void* x, int n, int decode, void* y_f32,
+                          void* cuda_stream) {
+    hi_status r = check_layer(m, layer_idx, w, x);
+    if (r != HI_OK) return r;
+    if (!y_f32 || n < 1 || n > m->ci.chunk || (decode && n != 1))
+        return hl_fail(m, HI_ESHAPE, "y_f32 NULL, n_tokens outside [1, chunk], or decode with n != 1");
+    hi::DeviceGuard dg(m->ci.device);
+    // x is read, not written: rmsnorm reads it; the residual add happens in hl_mlp_partial after the all-reduce
+    __nv_bfloat16* xb = const_cast<__nv_bfloat16*>(static_cast<const __nv_bfloat16*>(x));
+    return attn_half(m, layer_idx, w, xb, n, static_cast<float*>(y_f32), static_cast<cudaStream_t>(cuda_stream), [&] {
+        return decode ? hi_decode(m->ctx, layer_idx, m->q, m->k, m->v, m->attn, cuda_stream)
+                      : hi_prefill_chunk(m->ctx, layer_idx, m->q, m->k, m->v, m->attn, n, cuda_stream);
+    });
+}
+
+hi_status hl_mlp_partial(hl_model* m, int layer_idx, const hl_weights* w, void* x, const void* y_f32, int n, void* z_f32,
+                         void* cuda_stream) {
+    hi_status r = check_layer(m, layer_idx, w, x);
+    if (r != HI_OK) return r;
+    if (!y_f32 || !z_f32 || n < 1 || n > m->ci.chunk) return hl_fail(m, HI_ESHAPE, "NULL partial or n_tokens out of range");
+    hi::DeviceGuard dg(m->ci.device);
+    const cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    __nv_bfloat16* xb = static_cast<__nv_bfloat16*>(x);
+    if ((r = residual_add(m, xb, static_cast<const float*>(y_f32), n, st)) != HI_OK) return r;
+    return mlp_half(m, w, xb, n, static_cast<float*>(z_f32), st);
+}
+
+hi_status hl_residual_add(hl_model* m, void* x, const void* z_f32, int n, void* cuda_stream) {
+    if (!m) return HI_ESHAPE;
+    if (!x || !z_f32 || n < 1) return hl_fail(m, HI_ESHAPE, "NULL tensor or n < 1");
+    hi::DeviceGuard dg(m->ci.device);
+    return residual_add(m, static_cast<__nv_bfloat16*>(x), static_cast<const float*>(z_f32), n,
+                        static_cast<cudaStream_t>(cuda_stream));
+}
+
 hi_status hl_gemm(const void* w, const void* x, void* y, int mo, int n, int kd, int beta, void* cuda_stream) {
     if (!w || !x || !y || mo <= 0 || n <= 0 || kd <= 0 || mo % 64 || kd % 8)
         return hl_fail(nullptr, HI_EINVAL, "hl_gemm: NULL pointer or sizes (mo % 64, kd % 8)");
     const cudaError_t e = hi::launch_gemm(static_cast<const __nv_bfloat16*>(w), static_cast<const __nv_bfloat16*>(x),
-                                          static_cast<__nv_bfloat16*>(y), mo, n, kd, beta ? 1 : 0,
-                                          static_cast<cudaStream_t>(cuda_stream));
+                                          y, mo, n, kd, beta ? 1 : 0, 0, static_cast<cudaStream_t>(cuda_stream));
     if (e != cudaSuccess) {
         cudaGetLastError();
         return hl_fail(nullptr, HI_ECUDA, std::string("hl_gemm: ") + cudaGetErrorString(e));

@@ -14,6 +14,8 @@
 //
 // gemv_kernel (n == 1, decode): HBM-bound: each warp streams 2 weight rows with 16-byte loads against x held
 // in shared memory (fp32), warp-shuffle reduction, one rounding per output (+ residual).
+// Both also write fp32 outputs without rounding (`out_f32`): the partial sums of a tensor-parallel layer, which
+// are all-reduced across ranks before the residual add rounds once.
 #include "hi_kernels.cuh"
 #include "tc_ptx.cuh"
 
@@ -51,9 +53,10 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
     nb = local / gm;
 }
 
+template <bool F32OUT>
 __global__ void __launch_bounds__(G_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
-                   __nv_bfloat16* __restrict__ y, int n, int mo, int kd, int beta) {
+                   void* __restrict__ yv, int n, int mo, int kd, int beta) {
     extern __shared__ uint8_t g_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(g_raw) + 1023) & ~uintptr_t(1023));
     GemmBars* bars = reinterpret_cast<GemmBars*>(smem + G_STAGES * STAGE_BYTES);
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             tc_fence_after();
             const int row = mb * GM + r_in;
             const bool live = row < n;
-            __nv_bfloat16* yr = y + static_cast<int64_t>(row) * mo + nb * GN;
+            const int64_t yoff = static_cast<int64_t>(row) * mo + nb * GN;
             const uint32_t taddr = tmem + b * GN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
             for (int c = 0; c < GN / 32; ++c) {
@@ -145,8 +148,14 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 tmem_ld32(taddr + c * 32, v);
                 tmem_wait_ld();
                 const int col = nb * GN + c * 32;
-                if (live && col < mo) {   // mo is a multiple of 64: a 32-column chunk is all in or all out
-                    uint4* dst = reinterpret_cast<uint4*>(yr + c * 32);
+                if (F32OUT && live && col < mo) {   // fp32 partial sums (tensor-parallel layer): no rounding here
+                    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(yv) + yoff + c * 32);
+#pragma unroll
+                    for (int e4 = 0; e4 < 8; ++e4)
+                        dst[e4] = make_float4(__uint_as_float(v[4 * e4]), __uint_as_float(v[4 * e4 + 1]),
+                                              __uint_as_float(v[4 * e4 + 2]), __uint_as_float(v[4 * e4 + 3]));
+                } else if (live && col < mo) {   // mo is a multiple of 64: a 32-column chunk is all in or all out
+                    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(yv) + yoff + c * 32);
                     float f[32];
 #pragma unroll
                     for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(v[e]);
@@ -189,9 +198,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 // y[o] = (beta ? y[o] : 0) + x . W[o, :]; 8 warps per CTA, 2 output rows per warp, x staged in shared memory
 constexpr int GV_WARPS = 8, GV_ROWS = 2;
 
+template <bool F32OUT>
 __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const __nv_bfloat16* __restrict__ w,
                                                              const __nv_bfloat16* __restrict__ x,
-                                                             __nv_bfloat16* __restrict__ y, int mo, int kd, int beta) {
+                                                             void* __restrict__ yv, int mo, int kd, int beta) {
     extern __shared__ float xs[];   // [kd]
     for (int i = threadIdx.x; i < kd; i += blockDim.x) xs[i] = __bfloat162float(x[i]);
     __syncthreads();
@@ -222,28 +232,31 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const __nv_bfloat16
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
         if (lane == 0 && o0 + r < mo) {
-            const float base = beta ? __bfloat162float(y[o0 + r]) : 0.f;
-            y[o0 + r] = __float2bfloat16_rn(base + acc[r]);
+            if constexpr (F32OUT) {
+                static_cast<float*>(yv)[o0 + r] = acc[r];
+            } else {
+                __nv_bfloat16* y = static_cast<__nv_bfloat16*>(yv);
+                const float base = beta ? __bfloat162float(y[o0 + r]) : 0.f;
+                y[o0 + r] = __float2bfloat16_rn(base + acc[r]);
+            }
         }
     }
 }
 
-}  // namespace
-
-cudaError_t launch_gemm(const __nv_bfloat16* w, const __nv_bfloat16* x, __nv_bfloat16* y, int mo, int n, int kd, int beta,
-                        cudaStream_t stream) {
-    if (mo <= 0 || n <= 0 || kd <= 0 || mo % 64 || kd % 8) return cudaErrorInvalidValue;
+template <bool F32OUT>
+cudaError_t launch_gemm_t(const __nv_bfloat16* w, const __nv_bfloat16* x, void* y, int mo, int n, int kd, int beta,
+                          cudaStream_t stream) {
     if (n == 1) {
         const int rows_per_cta = GV_WARPS * GV_ROWS;
         const size_t smem = static_cast<size_t>(kd) * sizeof(float);
         static std::atomic<unsigned long long> configured{0};
         if (smem > 48 * 1024)
-            if (cudaError_t e = set_smem_attr_once(gemv_kernel, 227 * 1024, configured); e != cudaSuccess) return e;
-        gemv_kernel<<<(mo + rows_per_cta - 1) / rows_per_cta, GV_WARPS * 32, smem, stream>>>(w, x, y, mo, kd, beta);
+            if (cudaError_t e = set_smem_attr_once(gemv_kernel<F32OUT>, 227 * 1024, configured); e != cudaSuccess) return e;
+        gemv_kernel<F32OUT><<<(mo + rows_per_cta - 1) / rows_per_cta, GV_WARPS * 32, smem, stream>>>(w, x, y, mo, kd, beta);
         return cudaGetLastError();
     }
     static std::atomic<unsigned long long> configured{0};
-    if (cudaError_t e = set_smem_attr_once(gemm_tc_kernel, G_SMEM, configured); e != cudaSuccess) return e;
+    if (cudaError_t e = set_smem_attr_once(gemm_tc_kernel<F32OUT>, G_SMEM, configured); e != cudaSuccess) return e;
     CUtensorMap tx, tw;
     {
         const cuuint64_t dims[2] = {static_cast<cuuint64_t>(kd), static_cast<cuuint64_t>(n)};
@@ -260,8 +273,16 @@ cudaError_t launch_gemm(const __nv_bfloat16* w, const __nv_bfloat16* x, __nv_bfl
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = ((n + GM - 1) / GM) * ((mo + GN - 1) / GN);
-    gemm_tc_kernel<<<tiles < sms ? tiles : sms, G_THREADS, G_SMEM, stream>>>(tx, tw, y, n, mo, kd, beta);
+    gemm_tc_kernel<F32OUT><<<tiles < sms ? tiles : sms, G_THREADS, G_SMEM, stream>>>(tx, tw, y, n, mo, kd, beta);
     return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_gemm(const __nv_bfloat16* w, const __nv_bfloat16* x, void* y, int mo, int n, int kd, int beta,
+                        int out_f32, cudaStream_t stream) {
+    if (mo <= 0 || n <= 0 || kd <= 0 || mo % 64 || kd % 8 || (out_f32 && beta)) return cudaErrorInvalidValue;
+    return out_f32 ? launch_gemm_t<true>(w, x, y, mo, n, kd, 0, stream) : launch_gemm_t<false>(w, x, y, mo, n, kd, beta, stream);
 }
 
 }  // namespace hi

@@ -189,10 +189,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = p.g;
     const int n_rows = p.n_q * g;
-    // causal segment: CTA x's work grows with its rows, so the grid runs longest-first (LPT) -- the short
-    // CTAs fill the tail instead of the long ones starting last
-    const bool lpt = p.flags & PF_CAUSAL;
-    const int row0 = (lpt ? static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x)) * (2 * BM);
+    // causal segment: CTA x's work grows with its rows, so the launcher sets row_rev = grid - 1 and the grid runs
+    // longest-first (LPT): the short CTAs fill the tail instead of the long ones starting last
+    const int row0 = abs(p.row_rev - static_cast<int>(blockIdx.x)) * (2 * BM);
     const int hh = blockIdx.y;                 // kv head within the launch's head group (state index)
     const int hq = p.head_q[hh], hk = p.head_kv[hh];  // its q/out columns and k/v coordinate (head maps)
     float* const o_acc = p.o_acc + static_cast<int64_t>(hh) * p.state_rows * D;
@@ -962,7 +961,9 @@ cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
         if (!make_tmap_bf16(&tk, p.k, 3, dims, strides, box)) return cudaErrorInvalidValue;
         if (!make_tmap_bf16(&tv, p.v, 3, dims, strides, box)) return cudaErrorInvalidValue;
     }
-    prefill_tc_kernel<D><<<dim3(grid, heads), NUM_THREADS, Smem<D>::ALLOC, stream>>>(tq, tk, tv, p);
+    PrefillParams pl = p;
+    pl.row_rev = (p.flags & PF_CAUSAL) ? grid - 1 : 0;
+    prefill_tc_kernel<D><<<dim3(grid, heads), NUM_THREADS, Smem<D>::ALLOC, stream>>>(tq, tk, tv, pl);
     return cudaGetLastError();
 }
 

@@ -31,7 +31,7 @@ class HeadInferLayer:
         self._wcache = {}
 
     def _weights(self, w: dict) -> hl_weights:
-        hq, hkv, d, H, I = self.hi.hq_loc, self.hi.hkv_loc, self.hi.head_dim, self.hidden, self.inter
+        hq, hkv, d, H, I = self.hi.hq_loc, self.hi.hkv_loc, self.hi.head_dim, self.hidden, self.inter // self.hi.world
         shapes = {"attn_norm": (H,), "w_qkv": ((hq + 2 * hkv) * d, H), "w_o": (H, hq * d), "mlp_norm": (H,),
                   "w_gate_up": (2 * I, H), "w_down": (H, I)}
         return hl_weights(**{k: _dev_tensor(w[k], shapes[k], k) for k in WEIGHT_NAMES})
@@ -53,6 +53,40 @@ class HeadInferLayer:
         ptr = _dev_tensor(x, (self.hidden,), "x")
         ws = self._weights(w)
         self._check(_lib.load().hl_decode(self._m, layer, ctypes.byref(ws), ptr, _stream_ptr(stream)))
+        return x
+
+    # -- tensor parallel (context world > 1; include/hilayer.h): the caller all-reduces y and z between the calls
+    def attn_partial(self, layer: int, w: dict, x: torch.Tensor, decode: bool = False, y: Optional[torch.Tensor] = None,
+                     stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """x [n, hidden] bf16 (read); returns y [n, hidden] fp32 = this rank's attention output times W_o^T."""
+        n = 1 if decode else x.shape[0]
+        xp = _dev_tensor(x, (n, self.hidden) if not decode or x.dim() == 2 else (self.hidden,), "x")
+        if y is None:
+            y = torch.empty((n, self.hidden), dtype=torch.float32, device=x.device)
+        ws = self._weights(w)
+        self._check(_lib.load().hl_attn_partial(self._m, layer, ctypes.byref(ws), xp, n, 1 if decode else 0,
+                                                y.data_ptr(), _stream_ptr(stream)))
+        return y
+
+    def mlp_partial(self, layer: int, w: dict, x: torch.Tensor, y: torch.Tensor, z: Optional[torch.Tensor] = None,
+                    stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """x = bf16(x + y) in place (y: the all-reduced attention partials); returns z fp32 = this rank's MLP partial."""
+        n = y.shape[0]
+        xp = _dev_tensor(x, (n, self.hidden) if x.dim() == 2 else (self.hidden,), "x")
+        if y.dtype != torch.float32 or not y.is_contiguous() or tuple(y.shape) != (n, self.hidden):
+            raise ValueError("y must be contiguous fp32 [n, hidden]")
+        if z is None:
+            z = torch.empty_like(y)
+        ws = self._weights(w)
+        self._check(_lib.load().hl_mlp_partial(self._m, layer, ctypes.byref(ws), xp, y.data_ptr(), n, z.data_ptr(),
+                                               _stream_ptr(stream)))
+        return z
+
+    def residual_add(self, x: torch.Tensor, z: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """x = bf16(x + z) (z: the all-reduced MLP partials)."""
+        n = z.shape[0]
+        xp = _dev_tensor(x, (n, self.hidden) if x.dim() == 2 else (self.hidden,), "x")
+        self._check(_lib.load().hl_residual_add(self._m, xp, z.data_ptr(), n, _stream_ptr(stream)))
         return x
 
     def close(self) -> None:
@@ -81,3 +115,25 @@ def hl_gemm(w: torch.Tensor, x: torch.Tensor, y: torch.Tensor, beta: bool = Fals
     if st != _lib.HI_OK:
         raise _lib.HIError(st, _lib.load().hl_last_error(None).decode(errors="replace"))
     return y
+
+
+def shard_layer_weights(w: dict, q_heads: int, kv_heads: int, head_dim: int, inter: int, rank: int, world: int) -> dict:
+    """Rank `rank`'s tensor-parallel shard of one layer's full weights (include/hilayer.h): the q/k/v rows and
+    W_o columns of its head shard (parallel.shard), its inter/world gate, up and down columns; norms replicated.
+    Slicing only (copies), no arithmetic."""
+    from .parallel import shard
+    sh = shard(q_heads, kv_heads, rank, world)
+    (q0, q1), (k0, k1) = sh["q"], sh["kv"]
+    d = head_dim
+    qkv = w["w_qkv"]
+    ko = q_heads * d
+    vo = ko + kv_heads * d
+    il = inter // world
+    i0 = rank * il
+    return {
+        "attn_norm": w["attn_norm"], "mlp_norm": w["mlp_norm"],
+        "w_qkv": torch.cat([qkv[q0 * d:q1 * d], qkv[ko + k0 * d:ko + k1 * d], qkv[vo + k0 * d:vo + k1 * d]]).contiguous(),
+        "w_o": w["w_o"][:, q0 * d:q1 * d].contiguous(),
+        "w_gate_up": torch.cat([w["w_gate_up"][i0:i0 + il], w["w_gate_up"][inter + i0:inter + i0 + il]]).contiguous(),
+        "w_down": w["w_down"][:, i0:i0 + il].contiguous(),
+    }

@@ -49,3 +49,27 @@ def to_token_major(gathered: torch.Tensor) -> torch.Tensor:
         return gathered.permute(1, 0, 2, 3).reshape(n, w * hq_loc, d)
     w, hq_loc, d = gathered.shape
     return gathered.reshape(w * hq_loc, d)
+
+
+def all_reduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place sum over the group (NCCL over NVLink on a GPU box; through host memory when the group is gloo
+    and the tensor lives on a GPU -- the ranks-share-one-GPU validation mode)."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+        return t
+    dist.all_reduce(t, group=group)
+    return t
+
+
+def tp_layer_step(layer, idx: int, w: dict, x: torch.Tensor, group=None, decode: bool = False,
+                  bufs: dict | None = None) -> torch.Tensor:
+    """One tensor-parallel decoder layer (include/hilayer.h): the library computes this rank's fp32 partials of
+    the O and down projections; the two all-reduces between its three calls are the only collectives."""
+    y = layer.attn_partial(idx, w, x, decode=decode, y=None if bufs is None else bufs.get("y"))
+    all_reduce_sum(y, group)
+    z = layer.mlp_partial(idx, w, x, y, z=None if bufs is None else bufs.get("z"))
+    all_reduce_sum(z, group)
+    layer.residual_add(x, z)
+    return x
