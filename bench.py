@@ -308,9 +308,9 @@ def run_ours(args, rank, world, local_rank, pg):
         model = HeadInferLayer(hi, H, I, MODEL_ROPE_THETA, MODEL_RMS_EPS)
         weights = []
         for l in range(L):   # full weights per layer, then this rank's tensor-parallel shard (world > 1)
-            wl = gen_layer_weights_cuda(SEED, l, H, I, hq, hkv, d)
-            weights.append(wl if hw == 1 else shard_layer_weights(wl, hq, hkv, d, I, hr, hw))
-            del wl
+            wfull = gen_layer_weights_cuda(SEED, l, H, I, hq, hkv, d)
+            weights.append(wfull if hw == 1 else shard_layer_weights(wfull, hq, hkv, d, I, hr, hw))
+            del wfull
         torch.cuda.synchronize()
         tp_bufs = {"y": torch.empty((c, H), dtype=torch.float32, device="cuda"),
                    "z": torch.empty((c, H), dtype=torch.float32, device="cuda")} if world > 1 else None
