@@ -120,6 +120,9 @@ typedef struct hi_options {
                                           FIRST history block of every offloaded unit (when a call has >= 2 blocks);
                                           the parity bar (relative L2 per q head) must FAIL where the absolute bounds
                                           alone cannot see it (near-uniform attention at long context) */
+#define HI_FLAG_PREFILL_PSMEM 0x1000   /* variants build only: the prefill kernel with P staged in shared memory
+                                          (variants/k_prefill_tcp.cu): S(j+1) overlaps the softmax of S(j); parity-green
+                                          but 18 % slower per launch (measured; the SS PV MMA doubles shared-memory reads) */
 #define HI_FLAG_FAULT_LAUNCH 0x200   /* FAULT INJECTION, tests only: the second hi_prefill_chunk / hi_decode call of the
                                         context makes a kernel launch with an invalid configuration (a synchronous
                                         CUDA error; the CUDA context survives), so the context must turn sticky */

@@ -28,6 +28,7 @@ HI_FLAG_FAULT_SKIP_RAW = 0x100
 HI_FLAG_FAULT_LAUNCH = 0x200
 HI_FLAG_FAULT_TRAP = 0x400
 HI_FLAG_FAULT_SKIP_BLOCK = 0x800
+HI_FLAG_PREFILL_PSMEM = 0x1000
 HI_RESIDENT_AUTO = -1
 HI_GROUP_AUTO = -1
 HI_GROUP_PAPER = -2

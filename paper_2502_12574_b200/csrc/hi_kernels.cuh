@@ -106,6 +106,8 @@ inline void set_identity_heads(PrefillParams& p, int n) {
 // the product path; k_prefill_tc2.cu: CTA pairs (cta_group::2, M = 256), head_dim 128, HI_FLAG_PREFILL_2CTA
 cudaError_t launch_prefill_tc2(const PrefillParams& p, int d, cudaStream_t stream);
 cudaError_t launch_prefill_tc(const PrefillParams& p, int d, cudaStream_t stream);
+// variants/k_prefill_tcp.cu (variants build only): the same contract with P staged in shared memory
+cudaError_t launch_prefill_tcp(const PrefillParams& p, int d, cudaStream_t stream);
 // k_prefill_tc1.cu: one CTA per 128 rows, three S buffers in TMEM, K/V multicast to CTA pairs
 cudaError_t launch_prefill_tc1(const PrefillParams& p, int d, cudaStream_t stream);
 // baseline comparator: mma.sync m16n8k16 (k_prefill_mma.cu), selected by HI_FLAG_MMA_SYNC_PREFILL

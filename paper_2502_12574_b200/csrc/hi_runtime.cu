@@ -338,6 +338,13 @@ cudaError_t launch_prefill(hi_ctx* c, const hi::PrefillParams& p) {
         return cudaSuccess;
     }
 #endif
+#ifdef HI_WITH_VARIANTS
+    // comparison kernel with P staged in shared memory (variants/k_prefill_tcp.cu), every head in one launch
+#ifndef HI_PSMEM_DEFAULT
+#define HI_PSMEM_DEFAULT 0
+#endif
+    if (HI_PSMEM_DEFAULT || (c->flags & HI_FLAG_PREFILL_PSMEM)) return hi::launch_prefill_tcp(p, c->d, c->s_comp);
+#endif
     // the product kernel: every head of the unit in one launch (grid.y, head maps)
     return hi::launch_prefill_tc(p, c->d, c->s_comp);
 }
@@ -589,8 +596,8 @@ hi_status hi_init_ex(int layers, int q_heads, int kv_heads, int head_dim, int64_
         return HI_EINVAL;
     }
 #ifndef HI_WITH_VARIANTS
-    if (o.flags & (HI_FLAG_MMA_SYNC_PREFILL | HI_FLAG_PREFILL_2CTA | HI_FLAG_PREFILL_TC1)) {
-        g_init_error = "the comparison prefill kernels (mma.sync, CTA pair, one tile) are only in the variants "
+    if (o.flags & (HI_FLAG_MMA_SYNC_PREFILL | HI_FLAG_PREFILL_2CTA | HI_FLAG_PREFILL_TC1 | HI_FLAG_PREFILL_PSMEM)) {
+        g_init_error = "the comparison prefill kernels (mma.sync, CTA pair, one tile, P in shared memory) are only in the variants "
                        "build (paper_2502_12574_b200.build.build_variant(\"cmp\", []), HI_LIB_VARIANT=cmp)";
         return HI_EINVAL;
     }

@@ -91,7 +91,7 @@ def test_init_rejects_invalid_options(lib, opts):
     assert b"hi_options" in lib.hi_last_error(None)
 
 
-@pytest.mark.parametrize("flags", [0x10, 0x20, 0x40])
+@pytest.mark.parametrize("flags", [0x10, 0x20, 0x40, 0x1000])
 def test_product_build_rejects_comparison_kernel_flags(lib, flags):
     """The comparison prefill kernels (mma.sync, CTA pair, one tile) live only in the variants build; the
     product library refuses their flags before touching CUDA."""

@@ -85,3 +85,18 @@ def test_one_tile_kernel_special(dist):
     ref, _ = run_oracle(r)
     compare(gpu, ref)
     ctx.close()
+
+
+@need_variant
+@pytest.mark.parametrize("dist", ["P", "S"])
+@pytest.mark.parametrize("g,d", [(1, 64), (4, 128), (8, 128)])
+def test_psmem_kernel(dist, g, d):
+    """The P-in-shared-memory prefill kernel behind HI_FLAG_PREFILL_PSMEM (variants/k_prefill_tcp.cu): ragged
+    causal chunks, many history blocks, head groups."""
+    r = Run(layers=2, q_heads=4 * g, kv_heads=4, d=d, chunks=[300, 300, 555, 77], n_decode=2, dist=dist,
+            opts=dict(slot_tokens=256, flags=0x1000, head_group=2))
+    gpu, ctx = run_gpu(r)
+    ref, inputs = run_oracle(r)
+    compare(gpu, ref)
+    check_host_kv(ctx, r, inputs)
+    ctx.close()
