@@ -11,11 +11,12 @@
 // releases the S columns as soon as S(j) is in registers (s_cons), the MMA warp issues S(j+1) right away, and
 // the softmax writes P(j) as bf16 into a per-tile shared-memory tile laid out exactly like a TMA SWIZZLE_128B
 // Q tile, from which PV(j) reads it as a K-major A operand (SS MMA).  The per-tile chain becomes
-// softmax(j) -> softmax(j+1) with the MMAs in its shadow; the price is 64 KiB of shared memory for P (so V gets
-// one stage, K two) and an SS instead of a TS PV MMA.
+// softmax(j) -> softmax(j+1) with the MMAs in its shadow; the price is 64 KiB of shared memory for P (K and V
+// share one 3-slot ring in consumption order) and an SS instead of a TS PV MMA.
 //
-// Pipeline (one thread issues every MMA):  S_A(0) S_B(0) | for j: S_A(j+1) S_B(j+1) PV_A(j) PV_B(j).
-// Barriers: k_full/k_empty (2 K stages), v_full/v_empty (1 V stage), per tile s_full (S(j) in TMEM),
+// Pipeline: one thread issues every MMA, event-driven: a tile's S(j+1) as soon as its softmax has read S(j) and
+// K(j+1) landed, its PV(j) as soon as P(j) is in shared memory and V(j) landed.
+// Barriers: kv_full/kv_empty (3-slot K/V ring), per tile s_full (S(j) in TMEM),
 // s_cons (S(j) read by the softmax), p_full (P(j) in shared memory, O corrected), pv_done (PV(j) complete:
 // the P tile may be rewritten and O may be rescaled).
 #include "../hi_kernels.cuh"
@@ -32,7 +33,7 @@ using namespace ptx;
 
 constexpr int BM = 128;            // query rows per tile (TMEM lanes)
 constexpr int BN = 128;            // keys per KV tile
-constexpr int KSTAGES = 2;         // K ring (V has one stage: shared memory holds Q, P, K and V tiles)
+constexpr int KV_SLOTS = 3;        // one ring of K and V tiles in consumption order K(0), [K(i+1), V(i)] ...
 constexpr int SOFTMAX_WARPS = 8;
 constexpr int WARP_TMA = 8, WARP_MMA = 9;
 constexpr int NUM_THREADS = 32 * 12;
@@ -41,8 +42,7 @@ constexpr float RESCALE_THRESHOLD = 8.0f;
 
 struct __align__(8) Barriers {
     uint64_t q_full;
-    uint64_t k_full[KSTAGES], k_empty[KSTAGES];
-    uint64_t v_full, v_empty;
+    uint64_t kv_full[KV_SLOTS], kv_empty[KV_SLOTS];
     uint64_t s_full[2], s_cons[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
 };
@@ -52,9 +52,8 @@ struct Smem {
     static constexpr int BOX = BM * 128;                 // [128 rows][64 bf16] SWIZZLE_128B = 16 KiB
     static constexpr int Q_OFF = 0;                      // 2 tiles x D/64 boxes
     static constexpr int P_OFF = Q_OFF + 2 * (D / 64) * BOX;   // 2 tiles x BN/64 boxes
-    static constexpr int K_OFF = P_OFF + 2 * (BN / 64) * BOX;  // KSTAGES x D/64 boxes
-    static constexpr int V_OFF = K_OFF + KSTAGES * (D / 64) * BOX;
-    static constexpr int BAR_OFF = V_OFF + (D / 64) * BOX;
+    static constexpr int KV_OFF = P_OFF + 2 * (BN / 64) * BOX;  // KV_SLOTS x D/64 boxes
+    static constexpr int BAR_OFF = KV_OFF + KV_SLOTS * (D / 64) * BOX;
     static constexpr int BYTES = BAR_OFF + static_cast<int>(sizeof(Barriers));
     static constexpr int ALLOC = BYTES + 1024;
 };
@@ -110,9 +109,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int n_kt = max(n_kt0, n_kt1);
 
     const uint32_t bar_q = smem_addr(&bars->q_full);
-    auto bar_kf = [&](int s) { return smem_addr(&bars->k_full[s]); };
-    auto bar_ke = [&](int s) { return smem_addr(&bars->k_empty[s]); };
-    const uint32_t bar_vf = smem_addr(&bars->v_full), bar_ve = smem_addr(&bars->v_empty);
+    auto bar_kvf = [&](int s) { return smem_addr(&bars->kv_full[s]); };
+    auto bar_kve = [&](int s) { return smem_addr(&bars->kv_empty[s]); };
+    // ring item of K(i) and of V(i): K(0), then K(i+1) before V(i); an item waits for the one 3 places earlier
+    auto item_k = [&](int i) { return i == 0 ? 0 : 2 * i - 1; };
+    auto item_v = [&](int i) { return i + 1 < n_kt ? 2 * i + 2 : 2 * i + 1; };
     auto bar_s = [&](int t) { return smem_addr(&bars->s_full[t]); };
     auto bar_sc = [&](int t) { return smem_addr(&bars->s_cons[t]); };
     auto bar_p = [&](int t) { return smem_addr(&bars->p_full[t]); };
@@ -120,12 +121,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
-        for (int s = 0; s < KSTAGES; ++s) {
-            mbar_init(bar_kf(s), 1);
-            mbar_init(bar_ke(s), 1);
+        for (int s = 0; s < KV_SLOTS; ++s) {
+            mbar_init(bar_kvf(s), 1);
+            mbar_init(bar_kve(s), 1);
         }
-        mbar_init(bar_vf, 1);
-        mbar_init(bar_ve, 1);
         for (int t = 0; t < 2; ++t) {
             mbar_init(bar_s(t), 1);
             mbar_init(bar_sc(t), 128);
@@ -153,20 +152,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int c = 0; c < D / 64; ++c)
                     tma_load_3d(sbase + L::Q_OFF + (tt * (D / 64) + c) * L::BOX, &tm_q, bar_q, c * 64, hq * g,
                                 (row0 + tt * BM) / g);
-            auto load_k = [&](int i) {
-                const int s = i % KSTAGES;
-                if (i >= KSTAGES) mbar_wait(bar_ke(s), ((i / KSTAGES) - 1) & 1);
-                mbar_expect_tx(bar_kf(s), (D / 64) * L::BOX);
+            auto load = [&](int item, const CUtensorMap* map, int i) {
+                const int s = item % KV_SLOTS;
+                if (item >= KV_SLOTS) mbar_wait(bar_kve(s), ((item / KV_SLOTS) - 1) & 1);
+                mbar_expect_tx(bar_kvf(s), (D / 64) * L::BOX);
                 for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sbase + L::K_OFF + (s * (D / 64) + c) * L::BOX, &tm_k, bar_kf(s), c * 64, kb + i * BN, hk);
+                    tma_load_3d(sbase + L::KV_OFF + (s * (D / 64) + c) * L::BOX, map, bar_kvf(s), c * 64, kb + i * BN, hk);
             };
-            load_k(0);
+            load(item_k(0), &tm_k, 0);
             for (int i = 0; i < n_kt; ++i) {
-                if (i + 1 < n_kt) load_k(i + 1);
-                if (i >= 1) mbar_wait(bar_ve, (i - 1) & 1);   // V(i-1) consumed by both tiles' PV
-                mbar_expect_tx(bar_vf, (D / 64) * L::BOX);
-                for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sbase + L::V_OFF + c * L::BOX, &tm_v, bar_vf, c * 64, kb + i * BN, hk);
+                if (i + 1 < n_kt) load(item_k(i + 1), &tm_k, i + 1);
+                load(item_v(i), &tm_v, i);
             }
         } else if (warp == WARP_MMA && lane == 0 && n_kt > 0) {
             // ============================ MMA issuer
@@ -174,12 +170,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
             const int nk_t[2] = {n_kt0, n_kt1};
             const uint64_t dq0 = sdesc(sbase + L::Q_OFF, 16, 1024);
-            const uint64_t dk0 = sdesc(sbase + L::K_OFF, 16, 1024);
+            const uint64_t dk0 = sdesc(sbase + L::KV_OFF, 16, 1024);
             const uint64_t dp0 = sdesc(sbase + L::P_OFF, 16, 1024);
-            const uint64_t dv0 = sdesc(sbase + L::V_OFF, L::BOX, 1024);
+            const uint64_t dv0 = sdesc(sbase + L::KV_OFF, L::BOX, 1024);
             auto issue_s = [&](int tt, int i) {   // S_tt(i) = Q_tt K(i)^T -> TMEM columns 256 tt
                 const uint64_t a0 = dq0 + ((tt * (D / 64) * L::BOX) >> 4);
-                const uint64_t b0 = dk0 + (((i % KSTAGES) * (D / 64) * L::BOX) >> 4);
+                const uint64_t b0 = dk0 + (((item_k(i) % KV_SLOTS) * (D / 64) * L::BOX) >> 4);
 #pragma unroll 1   // rolled: the issuer runs on 88 registers, and one MMA takes 64 cycles to execute
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
@@ -189,40 +185,54 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             };
             auto issue_pv = [&](int tt, int j) {  // O_tt += P_tt(j) V(j): A = P (shared, K-major), B = V (MN-major)
                 const uint64_t a0 = dp0 + ((tt * (BN / 64) * L::BOX) >> 4);
+                const uint64_t v0 = dv0 + (((item_v(j) % KV_SLOTS) * (D / 64) * L::BOX) >> 4);
 #pragma unroll 1
                 for (int kk = 0; kk < BN / 16; ++kk) {
                     const uint32_t aoff = ((kk >> 2) * L::BOX + (kk & 3) * 32) >> 4;
-                    umma_bf16(tmem + tt * 256 + 128, a0 + aoff, dv0 + ((kk * 16 * 128) >> 4), ID_O,
+                    umma_bf16(tmem + tt * 256 + 128, a0 + aoff, v0 + ((kk * 16 * 128) >> 4), ID_O,
                               (j > 0 || kk > 0 || !first) ? 1u : 0u);
                 }
                 umma_commit(bar_pv(tt));
             };
             mbar_wait(bar_q, 0);
-            mbar_wait(bar_kf(0), 0);
-            tc_fence_after();
-            for (int tt = 0; tt < n_tiles; ++tt)
-                if (nk_t[tt] > 0) issue_s(tt, 0);
-            umma_commit(bar_ke(0));
-            for (int j = 0; j < n_kt; ++j) {
-                if (j + 1 < n_kt) {   // S(j+1) of each tile as soon as its softmax holds S(j) in registers
-                    const int s1 = (j + 1) % KSTAGES;
-                    mbar_wait(bar_kf(s1), ((j + 1) / KSTAGES) & 1);
-                    for (int tt = 0; tt < n_tiles; ++tt) {
-                        if (j + 1 >= nk_t[tt]) continue;
-                        mbar_wait(bar_sc(tt), j & 1);
-                        tc_fence_after();
-                        issue_s(tt, j + 1);
+            // Event-driven issue: each tile's next S and next PV go to the tensor pipe as soon as their inputs are
+            // ready, whatever the other tile is doing (a fixed S_A S_B PV_A PV_B order made each tile's S wait on
+            // the other tile's P).  A ring slot is released when the last tile that reads it has issued its MMA;
+            // the tiles cannot drift more than a few KV tiles apart (the ring holds 3), so 4 counters suffice.
+            int ns[2] = {0, 0}, npv[2] = {0, 0};
+            uint32_t kmask = 0, vmask = 0;   // bit (i & 3): one of two reading tiles has issued on K(i) / V(i)
+            // true when this issue is the last read of the item (then its ring slot is released)
+            auto last_user = [&](uint32_t& mask, int i) {
+                if ((i < nk_t[0]) != (i < nk_t[1])) return true;   // only one tile reads it
+                const uint32_t bit = 1u << (i & 3);
+                const bool second = mask & bit;
+                mask ^= bit;
+                return second;
+            };
+            while (npv[0] < nk_t[0] || npv[1] < nk_t[1]) {
+#pragma unroll
+                for (int tt = 0; tt < 2; ++tt) {
+                    const int j = ns[tt];
+                    if (j < nk_t[tt] && (j == 0 || mbar_test(bar_sc(tt), (j - 1) & 1))) {   // S(j-1) read
+                        const int it = item_k(j);
+                        if (mbar_test(bar_kvf(it % KV_SLOTS), (it / KV_SLOTS) & 1)) {
+                            tc_fence_after();
+                            issue_s(tt, j);
+                            ns[tt] = j + 1;
+                            if (last_user(kmask, j)) umma_commit(bar_kve(it % KV_SLOTS));
+                        }
                     }
-                    umma_commit(bar_ke(s1));   // K(j+1) free once those MMAs completed
+                    const int jp = npv[tt];
+                    if (jp < ns[tt] && mbar_test(bar_p(tt), jp & 1)) {   // P(jp) in shared memory, O corrected
+                        const int iv = item_v(jp);
+                        if (mbar_test(bar_kvf(iv % KV_SLOTS), (iv / KV_SLOTS) & 1)) {
+                            tc_fence_after();
+                            issue_pv(tt, jp);
+                            npv[tt] = jp + 1;
+                            if (last_user(vmask, jp)) umma_commit(bar_kve(iv % KV_SLOTS));
+                        }
+                    }
                 }
-                mbar_wait(bar_vf, j & 1);
-                for (int tt = 0; tt < n_tiles; ++tt) {
-                    if (j >= nk_t[tt]) continue;
-                    mbar_wait(bar_p(tt), j & 1);   // P(j) in shared memory, O corrected
-                    tc_fence_after();
-                    issue_pv(tt, j);
-                }
-                umma_commit(bar_ve);   // V(j) free
             }
         }
     } else {
@@ -321,6 +331,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const float nm = (mref == -CUDART_INF_F) ? 0.f : -mref;
                 f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
                 const f2 sc2{sc, sc}, nm2{nm, nm};
+#ifdef HI_FAKE_SOFTMAX   // timing experiment only: the MMA / shared-memory ceiling of this pipeline without exps
+                if (true) {
+                } else
+#endif
 #pragma unroll
                 for (int i = 0; i < BN; i += 2) {
                     const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
