@@ -962,7 +962,11 @@ cudaError_t launch_tc(const PrefillParams& p, cudaStream_t stream) {
         if (!make_tmap_bf16(&tv, p.v, 3, dims, strides, box)) return cudaErrorInvalidValue;
     }
     PrefillParams pl = p;
+#ifndef HI_NO_LPT
     pl.row_rev = (p.flags & PF_CAUSAL) ? grid - 1 : 0;
+#else
+    pl.row_rev = 0;   // A/B: causal CTAs in launch order
+#endif
     prefill_tc_kernel<D><<<dim3(grid, heads), NUM_THREADS, Smem<D>::ALLOC, stream>>>(tq, tk, tv, pl);
     return cudaGetLastError();
 }
