@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {   // ---------------- MMA issuer
+        {   // ---------------- MMA issuer: the whole warp runs the loop, elect.sync issues (no waterfall per MMA)
             constexpr uint32_t IDESC = idesc_bf16(GM, GN, false);
             int it = 0, i = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
@@ -121,10 +121,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                     const uint64_t db = sdesc(sbase + s * STAGE_BYTES + A_BYTES, 16, 1024);
 #pragma unroll
                     for (int kk = 0; kk < GK / 16; ++kk)   // 32-byte steps inside the 128-byte swizzle atom
-                        umma_bf16(acc, da + (kk * 2), db + (kk * 2), IDESC, (k > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit(empty(s));   // the stage is free once these MMAs have read it
+                        umma_bf16_w(acc, da + (kk * 2), db + (kk * 2), IDESC, (k > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit_w(empty(s));   // the stage is free once these MMAs have read it
                 }
-                umma_commit(accf(b));        // accumulator complete
+                umma_commit_w(accf(b));        // accumulator complete
             }
         }
     } else {

@@ -75,6 +75,34 @@ constexpr int NUM_THREADS = 32 * (SOFTMAX_WARPS + 4);  // + one warpgroup: TMA w
 constexpr int REG_SOFTMAX = HI_REG_SOFTMAX;
 constexpr int REG_PRODUCER = HI_REG_PRODUCER;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+// HI_WARP_ISSUE: the MMA warp runs the issue loop with all 32 lanes and elect.sync picks the issuing lane inside
+// each tcgen05.mma / commit.  From a lane-0-only region ptxas wraps every UTCHMMA in a waterfall loop (ELECT,
+// R2UR.BROADCAST, BRA.U.ANY) whose cost per MMA is close to the 64 cycles an M128 N128 K16 MMA runs, so the
+// issuer throttled the tensor pipe: measured +5.3 % TFLOP/s (+10.7 % per clock) in the sustained 1M probe
+// (profiles/prefill_probe_r02.jsonl, 3 interleaved repetitions); a rolled issue loop, the other direction,
+// costs 12 %.  0 = the round-1 lane-0 issue.
+#ifndef HI_WARP_ISSUE
+#define HI_WARP_ISSUE 1
+#endif
+#if HI_WARP_ISSUE
+#define HI_UMMA umma_bf16_w
+#define HI_UMMA_TS umma_bf16_ts_w
+#define HI_UCOMMIT umma_commit_w
+#else
+#define HI_UMMA umma_bf16
+#define HI_UMMA_TS umma_bf16_ts
+#define HI_UCOMMIT umma_commit
+#endif
+// HI_ROLL_ISSUE: keep the MMA issuer's K-step loops rolled (fewer live descriptors: no spills at the 64 registers
+// the issuer gets with SPLIT = 2)
+#ifndef HI_ROLL_ISSUE
+#define HI_ROLL_ISSUE 0
+#endif
+#if HI_ROLL_ISSUE
+#define HI_ISSUE_UNROLL _Pragma("unroll 1")
+#else
+#define HI_ISSUE_UNROLL _Pragma("unroll")
+#endif
 
 // Optional timeline trace (variant builds with -DHI_TRACE): clock64() at pipeline events of CTA 0,
 // read back with hi_debug_prefill_trace(); off in the product build.
@@ -286,7 +314,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int c = 0; c < D / 64; ++c)
                     tma_load_3d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, kb + i * BN, hk);
             }
-        } else if (warp == WARP_MMA && lane == 0 && n_kt > 0) {
+        } else if (warp == WARP_MMA && (HI_WARP_ISSUE || lane == 0) && n_kt > 0) {
             // ============================ MMA issuer ==============================
             constexpr uint32_t ID_S = idesc_bf16(BM, BN, false);
             constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
@@ -302,13 +330,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint64_t a0 = dq0 + ((tt * (D / 64) * L::BOX) >> 4);
                 const uint64_t b0 = dk0 + ((s * (D / 64) * L::BOX) >> 4);
 #ifndef HI_SKIP_S  // timing experiment switch
-#pragma unroll
+                HI_ISSUE_UNROLL
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
-                    umma_bf16(tmem + tt * 256, a0 + off, b0 + off, ID_S, ks > 0);
+                    HI_UMMA(tmem + tt * 256, a0 + off, b0 + off, ID_S, ks > 0);
                 }
 #endif
-                umma_commit(bar_s(tt));
+                HI_UCOMMIT(bar_s(tt));
             };
             auto issue_pv = [&](int tt, int j) {  // O_tt += P_tt(j) V(j), P from TMEM
                 const int s = j % NS;
@@ -316,10 +344,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifndef HI_SKIP_PV  // timing experiment switch
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk)
-                    umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
+                    HI_UMMA_TS(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                  (j > 0 || kk > 0 || !first) ? 1u : 0u);
 #endif
-                if (j + 1 == nk_t[tt]) umma_commit(bar_o(tt));  // O final: the epilogue's only wait
+                if (j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));  // O final: the epilogue's only wait
             };
             mbar_wait(bar_k(0), 0);
             tc_fence_after();
@@ -331,18 +359,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 auto issue_s_half = [&](int tt, int i, int h) {
                     const uint64_t a0 = dq0 + ((tt * (D / 64) * L::BOX) >> 4);
                     const uint64_t b0 = dk0 + (((i % NS) * (D / 64) * L::BOX + h * 64 * 128) >> 4);
-#pragma unroll
+                    HI_ISSUE_UNROLL
                     for (int ks = 0; ks < D / 16; ++ks) {
                         const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
-                        umma_bf16(tmem + tt * 256 + 64 * h, a0 + off, b0 + off, ID_S64, ks > 0);
+                        HI_UMMA(tmem + tt * 256 + 64 * h, a0 + off, b0 + off, ID_S64, ks > 0);
                     }
                 };
                 // O_tt += P_tt(j)[keys 64h ..] V(j)[keys 64h ..]; P at packed columns 64 + 32h ..
                 auto issue_pv_half = [&](int tt, int j, int h) {
                     const uint64_t b0 = dv0 + (((j % NS) * (D / 64) * L::BOX) >> 4);
-#pragma unroll
+                    HI_ISSUE_UNROLL
                     for (int kk = (h ? KS / 16 : 0); kk < (h ? BN / 16 : KS / 16); ++kk)
-                        umma_bf16_ts(tmem + tt * 256 + 128, tmem + tt * 256 + P_COL + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
+                        HI_UMMA_TS(tmem + tt * 256 + 128, tmem + tt * 256 + P_COL + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                      (j > 0 || kk > 0 || !first) ? 1u : 0u);
                 };
                 for (int j = 0; j < n_kt; ++j) {
@@ -370,21 +398,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         HI_TR_MMA(12 + 2 * tt, j);
                         tc_fence_after();
                         issue_pv_half(tt, j, 1);
-                        if (j + 1 == nk_t[tt]) umma_commit(bar_o(tt));
+                        if (j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));
                         if (next) {
                             if (!have_k) { mbar_wait(bar_k((j + 1) % NS), ((j + 1) / NS) & 1); have_k = true; }
                             tc_fence_after();
                             if (SPLIT_S_LO) {
                                 if (!lo_done) issue_s_half(tt, j + 1, 0);
                                 issue_s_half(tt, j + 1, 1);
-                                umma_commit(bar_s(tt));
+                                HI_UCOMMIT(bar_s(tt));
                             } else {
                                 issue_s(tt, j + 1);  // commits s_full
                             }
                             HI_TR_MMA(12 + 2 * tt + 1, j);
                         }
                     }
-                    umma_commit(bar_e(s));  // K(j), V(j) consumed by every tile
+                    HI_UCOMMIT(bar_e(s));  // K(j), V(j) consumed by every tile
                 }
             } else {
             for (int j = 0; j < n_kt; ++j) {
@@ -404,7 +432,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         HI_TR_MMA(12 + 2 * tt + 1, j);
                     }
                 }
-                umma_commit(bar_e(s));  // K(j), V(j) consumed by every tile
+                HI_UCOMMIT(bar_e(s));  // K(j), V(j) consumed by every tile
             }
             }
         }
@@ -422,7 +450,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int rg = row0 + tt * BM + r;          // packed row index t*g + j
         const bool row_valid = rg < n_rows;
         const int t = row_valid ? rg / g : 0;
-        const int64_t qpos = p.q_pos0 + t;
+        // the row's global position; recomputed where the masks need it (keeping it live costs a spill)
+#define qpos (p.q_pos0 + t)
         const int nkt = tt == 0 ? n_kt0 : n_kt1;
         const int t_lo = (row0 + tt * BM) / g;
         const int t_hi_tile = min(p.n_q - 1, (row0 + tt * BM + BM - 1) / g);
@@ -925,6 +954,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
     }
+#undef qpos
     tc_fence_before();
     __syncthreads();
     if (warp == WARP_MMA) {
