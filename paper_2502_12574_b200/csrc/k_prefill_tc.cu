@@ -64,16 +64,18 @@ constexpr int NUM_THREADS = 32 * (SOFTMAX_WARPS + 4);  // + one warpgroup: TMA w
 // Register budget (setmaxnreg).  setmaxnreg.inc only draws on registers that setmaxnreg.dec released
 // in the same CTA (it blocks forever otherwise), so  softmax threads x (inc - launch)  must equal at
 // most  producer threads x (launch - dec):
-//   SPLIT=1: launch 168 x 384; softmax 208 (+40 x 256), producer 88 (-80 x 128)
+//   SPLIT=1, d=128: launch 168 x 384; softmax 208 (+40 x 256), producer 88 (-80 x 128)
+//   SPLIT=1, d=64:  softmax 216 (+48 x 256), producer 72 (-96 x 128): the d = 64 issuer needs fewer descriptor
+//                   registers and its softmax loop spills its counter at 208 (the d = 128 issuer spills at 72)
 //   SPLIT=2: launch  96 x 640; softmax 104 (+8 x 512), producer 64 (-32 x 128)
 #ifndef HI_REG_SOFTMAX
-#define HI_REG_SOFTMAX (SPLIT == 1 ? 208 : 104)
+#define HI_REG_SOFTMAX (SPLIT == 1 ? (D == 64 ? 216 : 208) : 104)
 #endif
 #ifndef HI_REG_PRODUCER
-#define HI_REG_PRODUCER (SPLIT == 1 ? 88 : 64)
+#define HI_REG_PRODUCER (SPLIT == 1 ? (D == 64 ? 72 : 88) : 64)
 #endif
-constexpr int REG_SOFTMAX = HI_REG_SOFTMAX;
-constexpr int REG_PRODUCER = HI_REG_PRODUCER;
+template <int D> constexpr int REG_SOFTMAX = HI_REG_SOFTMAX;
+template <int D> constexpr int REG_PRODUCER = HI_REG_PRODUCER;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 // HI_WARP_ISSUE: the MMA warp runs the issue loop with all 32 lanes and elect.sync picks the issuing lane inside
 // each tcgen05.mma / commit.  From a lane-0-only region ptxas wraps every UTCHMMA in a waterfall loop (ELECT,
@@ -179,6 +181,7 @@ struct __align__(8) Barriers {
     volatile int tile_done[2];    // PINGPONG: tile t has taken its last turn (its partner stops waiting for it)
     float xchg[2][2][BM];   // [tile][half][row]: partial row max, SPLIT=2
     float xchg_l[2][2][BM]; // [tile][half][row]: partial row sum (epilogue), SPLIT=2
+    int row_t[2][BM];       // [tile][row]: the row's chunk token t, re-read by the mask paths (a live copy spills)
 };
 
 template <int D>
@@ -192,11 +195,13 @@ struct Smem {
     static constexpr int ALLOC = BYTES + 1024;      // slack for 1 KiB alignment
 };
 
+template <int D>
 __device__ __forceinline__ void setmaxnreg_softmax() {
-    if constexpr (REG_SOFTMAX > (SPLIT == 1 ? 168 : 96)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_SOFTMAX));
+    if constexpr (REG_SOFTMAX<D> > (SPLIT == 1 ? 168 : 96)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REG_SOFTMAX<D>));
 }
+template <int D>
 __device__ __forceinline__ void setmaxnreg_producer() {
-    if constexpr (REG_PRODUCER < (SPLIT == 1 ? 168 : 96)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_PRODUCER));
+    if constexpr (REG_PRODUCER<D> < (SPLIT == 1 ? 168 : 96)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_PRODUCER<D>));
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tmem = bars->tmem_base;
 
     if (warp >= SOFTMAX_WARPS) {
-        setmaxnreg_producer();
+        setmaxnreg_producer<D>();
         if (warp == WARP_TMA && lane == 0 && n_kt > 0) {
             // ============================ TMA producer ============================
             mbar_expect_tx(bar_q, n_tiles * (D / 64) * L::BOX);
@@ -438,7 +443,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else {
         // ====================== softmax / correction / epilogue: warps 0-3 tile 0, 4-7 tile 1 ======================
-        setmaxnreg_softmax();
+        setmaxnreg_softmax<D>();
         const int tt = warp / (4 * SPLIT);
         const int hf = (warp / 4) % SPLIT;          // which BN/SPLIT S columns (and D/SPLIT O columns)
         const int wq = warp & 3;                    // TMEM lane quarter
@@ -450,8 +455,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int rg = row0 + tt * BM + r;          // packed row index t*g + j
         const bool row_valid = rg < n_rows;
         const int t = row_valid ? rg / g : 0;
-        // the row's global position; recomputed where the masks need it (keeping it live costs a spill)
-#define qpos (p.q_pos0 + t)
+        // the row's global position; the masks re-read t from shared memory (keeping it live costs a spill)
+        bars->row_t[tt][r] = t;  // SPLIT == 2: both warps of the row store the same value before reading it
+        volatile const int* const t_sm = &bars->row_t[tt][r];
+#define qpos (p.q_pos0 + *t_sm)
         const int nkt = tt == 0 ? n_kt0 : n_kt1;
         const int t_lo = (row0 + tt * BM) / g;
         const int t_hi_tile = min(p.n_q - 1, (row0 + tt * BM + BM - 1) / g);
