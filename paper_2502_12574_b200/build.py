@@ -38,7 +38,8 @@ def _nvcc_shared(out: str, srcs, extra=(), force=False, verbose=False, libs=()):
     if not force and not _stale(out, deps):
         return out
     objs = []
-    bdir = os.path.join(os.path.dirname(out), "build")
+    # one object directory per library: variant builds may run concurrently
+    bdir = os.path.join(os.path.dirname(out), "build", os.path.splitext(os.path.basename(out))[0])
     os.makedirs(bdir, exist_ok=True)
     procs = []
     for s in srcs:

@@ -112,7 +112,11 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 __device__ unsigned long long g_hi_trace[16][512];
 #define HI_TR(ev, j) do { if (blockIdx.x == 0 && (threadIdx.x & 127) == 0 && (j) < 512) g_hi_trace[ev][j] = clock64(); } while (0)
 #define HI_TR_MMA(ev, j) do { if (blockIdx.x == 0 && (j) < 512) g_hi_trace[ev][j] = clock64(); } while (0)
+// stamp once register v has arrived (a TMEM load completes through the scoreboard, not at tcgen05.wait::ld)
+#define HI_TR_DEP(ev, j, v) do { uint32_t z_; asm volatile("and.b32 %0, %1, 0;" : "=r"(z_) : "r"(v)); \
+    if (blockIdx.x == 0 && (threadIdx.x & 127) == 0 && (j) < 512) g_hi_trace[ev][j] = clock64() + z_; } while (0)
 #else
+#define HI_TR_DEP(ev, j, v) do { } while (0)
 #define HI_TR(ev, j) do { } while (0)
 #define HI_TR_MMA(ev, j) do { } while (0)
 #endif
@@ -202,6 +206,11 @@ __device__ __forceinline__ void setmaxnreg_softmax() {
 template <int D>
 __device__ __forceinline__ void setmaxnreg_producer() {
     if constexpr (REG_PRODUCER<D> < (SPLIT == 1 ? 168 : 96)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REG_PRODUCER<D>));
+}
+__device__ __forceinline__ int ld_shared_s32(uint32_t addr) {  // volatile: re-read where used, not kept live
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -457,8 +466,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int t = row_valid ? rg / g : 0;
         // the row's global position; the masks re-read t from shared memory (keeping it live costs a spill)
         bars->row_t[tt][r] = t;  // SPLIT == 2: both warps of the row store the same value before reading it
-        volatile const int* const t_sm = &bars->row_t[tt][r];
-#define qpos (p.q_pos0 + *t_sm)
+        // (SPLIT == 1: row_t[tt][r] is word threadIdx.x, re-derived at the use instead of kept in a register)
+#define qpos (p.q_pos0 + ld_shared_s32(smem_addr(&bars->row_t[0][0]) + 4u * (SPLIT == 1 ? threadIdx.x : tt * BM + r)))
         const int nkt = tt == 0 ? n_kt0 : n_kt1;
         const int t_lo = (row0 + tt * BM) / g;
         const int t_hi_tile = min(p.n_q - 1, (row0 + tt * BM + BM - 1) / g);
@@ -499,7 +508,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int cb = 0; cb < HN / 32; ++cb)
                     tmem_ld32(t_s + hf * HN + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[cb * 32]));
                 tmem_wait_ld();
-                HI_TR(ttr + 0, j);
+                HI_TR_DEP(ttr + 0, j, x[0] ^ x[HN - 1]);
                 // row max of the raw scores (scale > 0 commutes with max); masking where needed
                 const int key0 = kb + j * BN + hf * HN;
                 const int kt0 = kb + j * BN;  // first key of the tile
@@ -638,6 +647,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     continue;
                 }
                 if constexpr (SPLIT_S && SPLIT == 1) {
+#ifdef HI_FAKE_SOFTMAX  // timing experiment only: the pipeline without the softmax math (P = raw S bits)
+                    tc_fence_before();
+                    mbar_arrive(bar_pl(tt));
+                    mbar_arrive(bar_p(tt));
+                    continue;
+#endif
                     if constexpr (SPLIT_S_LO) {  // S(j) is in registers: columns 0-63 may take S(j+1)_lo
                         tc_fence_before();
                         mbar_arrive(bar_sc(tt));
