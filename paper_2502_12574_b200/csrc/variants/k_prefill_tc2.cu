@@ -36,6 +36,15 @@ constexpr int NS = 4;                // K/V stages (each CTA: 16 KiB of K + 16 K
 constexpr int NUM_THREADS = 384;
 constexpr int WARP_TMA = 8, WARP_MMA = 9;
 constexpr float RESCALE_THRESHOLD = 8.0f;
+// HI_WARP_ISSUE (as in k_prefill_tc.cu): the whole MMA warp runs the issue loop, elect.sync picks the lane
+#ifndef HI_WARP_ISSUE
+#define HI_WARP_ISSUE 1
+#endif
+#if HI_WARP_ISSUE
+#define umma_bf16_cg2 umma_bf16_cg2_w
+#define umma_bf16_ts_cg2 umma_bf16_ts_cg2_w
+#define umma_commit_cg2_mc umma_commit_cg2_mc_w
+#endif
 
 constexpr int QBOX = BM * 128;       // [128 rows][64 d] bf16 SW128 = 16 KiB
 constexpr int KBOX = (BN / 2) * 128; // [64 keys][64 d] = 8 KiB  (this CTA's half of the keys)
@@ -133,7 +142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                                     i * BN + static_cast<int>(rank) * (BN / 2));
                 tma_load_2d_cg2(sbase + V_OFF + s * VBOX, &tm_v, full_l, static_cast<int>(rank) * 64, i * BN);
             }
-        } else if (warp == WARP_MMA && lane == 0 && leader && n_kt > 0) {
+        } else if (warp == WARP_MMA && (HI_WARP_ISSUE || lane == 0) && leader && n_kt > 0) {
             // ============================ MMA issuer (leader CTA) ============================
             constexpr uint32_t ID_S = idesc_bf16(2 * BM, BN, false);  // M = 256 (pair), N = 128 keys
             constexpr uint32_t ID_O = idesc_bf16(2 * BM, D, true);    // M = 256, N = 128 dims

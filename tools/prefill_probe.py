@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--dist", default="U")
     ap.add_argument("--resident", action="store_true", help="every (layer, kv head) resident in HBM (no H2D)")
     ap.add_argument("--slot-tokens", type=int, default=0)
+    ap.add_argument("--flags", type=lambda v: int(v, 0), default=0, help="extra hi_init flags (e.g. 0x20: CTA-pair kernel)")
     a = ap.parse_args()
     import bench
     from paper_2502_12574_b200._lib import HI_FLAG_TIMING
@@ -39,7 +40,7 @@ def main():
     bench.DIST = a.dist
     L, hq, hkv, d, S, c = a.layers, 32, 8, 128, a.ctx, a.chunk
     p_last = S - c
-    hi = HeadInfer(L, hq, hkv, d, S + 8, c, flags=HI_FLAG_TIMING, head_group=a.group,
+    hi = HeadInfer(L, hq, hkv, d, S + 8, c, flags=HI_FLAG_TIMING | a.flags, head_group=a.group,
                    resident_kv_heads=-1 if a.resident else 0, slot_tokens=a.slot_tokens)
     bench.fill_history(hi, L, hkv, 0, d, p_last, torch, fill_)
     ins = [bench.gen_layer_inputs(l, p_last, c, hq, hkv, d, 0, 0, torch, fill_) for l in range(L)]
@@ -64,7 +65,7 @@ def main():
     st1 = hi.stats()
     ms = st1["prefill_attn_ms"] - st0["prefill_attn_ms"]
     fl = st1["prefill_attn_flops"] - st0["prefill_attn_flops"]
-    res = {"variant": os.environ.get("HI_LIB_VARIANT", "product"), "ctx": S, "group": a.group, "layers": L,
+    res = {"variant": os.environ.get("HI_LIB_VARIANT", "product") + (f"+0x{a.flags:x}" if a.flags else ""), "ctx": S, "group": a.group, "layers": L,
            "resident": a.resident, "slot_tokens": hi.stats()["slot_tokens"],
            "steps": steps, "kernel_tflops": round(fl / ms / 1e9, 1), "kernel_ms_per_step": round(ms / steps, 2),
            "launches_per_step": (st1["prefill_attn_launches"] - st0["prefill_attn_launches"]) / steps,
