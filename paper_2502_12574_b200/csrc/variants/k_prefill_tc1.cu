@@ -55,6 +55,10 @@ constexpr int NUM_THREADS = 384;
 // setmaxnreg: softmax 256 threads x +40 = producers 128 x -80 (launch 168 = 64K / 384)
 constexpr int REG_SOFTMAX = 208, REG_PRODUCER = 88;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+// HI_WARP_ISSUE (as in k_prefill_tc.cu): the whole MMA warp runs the issue loop, elect.sync picks the lane
+#ifndef HI_WARP_ISSUE
+#define HI_WARP_ISSUE 1
+#endif
 
 #if HI_T1_CL > 1
 #define HI_T1_CLUSTER_ATTR __cluster_dims__(HI_T1_CL, 1, 1)
@@ -63,6 +67,15 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #endif
 
 using namespace ptx;
+#if HI_WARP_ISSUE
+#define T1_UMMA umma_bf16_w
+#define T1_UMMA_TS umma_bf16_ts_w
+#define T1_UCOMMIT umma_commit_w
+#else
+#define T1_UMMA umma_bf16
+#define T1_UMMA_TS umma_bf16_ts
+#define T1_UCOMMIT umma_commit
+#endif
 
 // Optional timeline trace (variant builds with -DHI_TRACE): clock64() at pipeline events of CTA 0
 // (blockIdx 0,0), read back with hi_debug_prefill_trace1(); off in the product build.
@@ -219,7 +232,7 @@ __global__ void HI_T1_CLUSTER_ATTR __launch_bounds__(NUM_THREADS, 1)
                 if (i >= NV) mbar_wait(bar_ve(s), ((i / NV) - 1) & 1);
                 load_tile(&tm_v, L::V_OFF + s * (D / 64) * L::BOX, bar_v(s), i, D / 64);
             }
-        } else if (warp == WARP_MMA && lane == 0 && n_kt > 0) {
+        } else if (warp == WARP_MMA && (HI_WARP_ISSUE || lane == 0) && n_kt > 0) {
             // ============================ MMA issuer ==============================
             constexpr uint32_t ID_S = idesc_bf16(BM, BN, false);
             constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
@@ -232,25 +245,25 @@ __global__ void HI_T1_CLUSTER_ATTR __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
-                    umma_bf16(tmem + (i % NSB) * 128, dq0 + off, b0 + off, ID_S, ks > 0);
+                    T1_UMMA(tmem + (i % NSB) * 128, dq0 + off, b0 + off, ID_S, ks > 0);
                 }
-                umma_commit(bar_s(i % NSB));
+                T1_UCOMMIT(bar_s(i % NSB));
             };
             auto issue_pv = [&](int j) {  // O += P(j) V(j), P from TMEM buffer j % 3
                 const uint64_t b0 = dv0 + (((j % NV) * (D / 64) * L::BOX) >> 4);
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk)
-                    umma_bf16_ts(tmem + 384, tmem + (j % NSB) * 128 + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
+                    T1_UMMA_TS(tmem + 384, tmem + (j % NSB) * 128 + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                  (j > 0 || kk > 0 || !first) ? 1u : 0u);
-                umma_commit(bar_pvd(j & 1));
-                if (j + 1 == nk_own) umma_commit(bar_od);
+                T1_UCOMMIT(bar_pvd(j & 1));
+                if (j + 1 == nk_own) T1_UCOMMIT(bar_od);
             };
             // release a ring slot once every MMA reading it is issued (the commit fires on completion).
             // Cluster: the round must also have fully landed here (this CTA may not have needed it), and
             // the release goes to every CTA of the cluster.
             auto release = [&](uint32_t full, uint32_t empty, uint32_t parity) {
                 if constexpr (CL == 1) {
-                    umma_commit(empty);
+                    T1_UCOMMIT(empty);
                 } else {
                     mbar_wait(full, parity);
                     umma_commit_mc(empty, MASK);
