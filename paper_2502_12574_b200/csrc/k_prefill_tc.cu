@@ -95,6 +95,13 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #define HI_UMMA_TS umma_bf16_ts
 #define HI_UCOMMIT umma_commit
 #endif
+// HI_SUMCHECK=1 (A/B, off): on unmasked tiles the split schedule exponentiates against the running reference and
+// checks each half's row sum against 2^8 instead of taking the 128-key row max first (see the softmax).  Exact and
+// parity-green, but measured 9 % slower per clock (668 vs 730 TFLOP/s per GHz, profiles/prefill_probe_r02.jsonl,
+// job AH): without the max phase the two tiles' exponential phases collide on the MUFU more often.
+#ifndef HI_SUMCHECK
+#define HI_SUMCHECK 0
+#endif
 // HI_KV_JOINT=1 (A/B only): the producer loads K(i) only once V(i - NS) is released too, in K(i), V(i) order -- the
 // round-1 prefetch distance (one tile step for K) with the separate barriers
 #ifndef HI_KV_JOINT
@@ -187,6 +194,7 @@ constexpr int P_COL = SPLIT_S_LO ? 64 : 0;    // first packed P column
 #define HI_P_SPLIT_KEYS 64
 #endif
 constexpr int KS = HI_P_SPLIT_KEYS;
+constexpr bool SUMCHECK = HI_SUMCHECK != 0 && HI_SPLIT_S == 2 && !HI_PINGPONG && !HI_SPEC_SPLIT && HI_P_SPLIT_KEYS == 64;
 static_assert(KS == 64 || KS == 96, "P split at 64 or 96 keys");
 static_assert(SPLIT == 1 || !SPLIT_S || (KS == 64 && !SPLIT_S_LO), "two warps per row split P at their 64-key boundary");
 static_assert(!SPEC_SPLIT || (KS == 64 && HI_SPLIT_S == 2),
@@ -199,6 +207,7 @@ struct __align__(8) Barriers {
     uint64_t k_full[NS], v_full[NS], k_empty[NS], v_empty[NS];  // K and V stages are released separately
     uint64_t s_full[2], p_full[2], o_done[2];
     uint64_t s_cons[2], p_lo[2];  // split schedule: S(j) read into registers / P(j) keys 0-63 stored
+    uint64_t pv_lo[2];            // SUMCHECK: PV(j)_lo of tile t complete (a second-half rescale waits for it)
     uint64_t tok[2][4];           // PINGPONG: MUFU token for tile t's warp on SMSP q (arrived by the other tile)
     uint32_t tmem_base;
     volatile int tile_done[2];    // PINGPONG: tile t has taken its last turn (its partner stops waiting for it)
@@ -296,6 +305,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto bar_o = [&](int t) { return smem_addr(&bars->o_done[t]); };
     auto bar_sc = [&](int t) { return smem_addr(&bars->s_cons[t]); };
     auto bar_pl = [&](int t) { return smem_addr(&bars->p_lo[t]); };
+    auto bar_pvl = [&](int t) { return smem_addr(&bars->pv_lo[t]); };
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
@@ -313,6 +323,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(bar_o(t), 1);
             mbar_init(bar_sc(t), 128);
             mbar_init(bar_pl(t), 128 * SPLIT);
+            mbar_init(bar_pvl(t), 1);
             for (int q = 0; q < 4; ++q) mbar_init(smem_addr(&bars->tok[t][q]), 1);
         }
         // a tile without KV tiles never takes a turn (its partner must not wait for it)
@@ -328,7 +339,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = bars->tmem_base;
+    // the TMEM base is re-read from shared memory where each role needs it (one copy live across the role split
+    // spilled to local memory)
+#define tmem static_cast<uint32_t>(ld_shared_s32(smem_addr(&bars->tmem_base)))
 
     if (warp >= SOFTMAX_WARPS) {
         setmaxnreg_producer<D>();
@@ -363,6 +376,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         } else if (warp == WARP_MMA && (HI_WARP_ISSUE || lane == 0) && n_kt > 0) {
             // ============================ MMA issuer ==============================
+            const uint32_t tmem_m = tmem;  // read once: the issue loop must not wait on shared memory
             constexpr uint32_t ID_S = idesc_bf16(BM, BN, false);
             constexpr uint32_t ID_O = idesc_bf16(BM, D, true);
             const int nk_t[2] = {n_kt0, n_kt1};
@@ -380,7 +394,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 HI_ISSUE_UNROLL
                 for (int ks = 0; ks < D / 16; ++ks) {
                     const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
-                    HI_UMMA(tmem + tt * 256, a0 + off, b0 + off, ID_S, ks > 0);
+                    HI_UMMA(tmem_m + tt * 256, a0 + off, b0 + off, ID_S, ks > 0);
                 }
 #endif
                 HI_UCOMMIT(bar_s(tt));
@@ -391,7 +405,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifndef HI_SKIP_PV  // timing experiment switch
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk)
-                    HI_UMMA_TS(tmem + tt * 256 + 128, tmem + tt * 256 + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
+                    HI_UMMA_TS(tmem_m + tt * 256 + 128, tmem_m + tt * 256 + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                  (j > 0 || kk > 0 || !first) ? 1u : 0u);
 #endif
                 if (j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));  // O final: the epilogue's only wait
@@ -412,7 +426,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     HI_ISSUE_UNROLL
                     for (int ks = 0; ks < D / 16; ++ks) {
                         const uint32_t off = ((ks >> 2) * L::BOX + (ks & 3) * 32) >> 4;
-                        HI_UMMA(tmem + tt * 256 + 64 * h, a0 + off, b0 + off, ID_S64, ks > 0);
+                        HI_UMMA(tmem_m + tt * 256 + 64 * h, a0 + off, b0 + off, ID_S64, ks > 0);
                     }
                 };
                 // O_tt += P_tt(j)[keys 64h ..] V(j)[keys 64h ..]; P at packed columns 64 + 32h ..
@@ -420,7 +434,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint64_t b0 = dv0 + (((j % NS) * (D / 64) * L::BOX) >> 4);
                     HI_ISSUE_UNROLL
                     for (int kk = (h ? KS / 16 : 0); kk < (h ? BN / 16 : KS / 16); ++kk)
-                        HI_UMMA_TS(tmem + tt * 256 + 128, tmem + tt * 256 + P_COL + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
+                        HI_UMMA_TS(tmem_m + tt * 256 + 128, tmem_m + tt * 256 + P_COL + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                      (j > 0 || kk > 0 || !first) ? 1u : 0u);
                 };
                 for (int j = 0; j < n_kt; ++j) {
@@ -444,6 +458,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (!waited_v) { MMA_WAIT(bar_v(s), (j / NS) & 1); waited_v = true; }
                         tc_fence_after();
                         issue_pv_half(tt, j, 0);
+                        if constexpr (SUMCHECK) HI_UCOMMIT(bar_pvl(tt));  // PV(j)_lo done (a rare second-half rescale)
                         MMA_WAIT(bar_p(tt), j & 1);
                         HI_TR_MMA(12 + 2 * tt, j);
                         tc_fence_after();
@@ -505,7 +520,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // the row's global position; the masks re-read t from shared memory (keeping it live costs a spill)
         bars->row_t[tt][r] = t;  // SPLIT == 2: both warps of the row store the same value before reading it
         // (SPLIT == 1: row_t[tt][r] is word threadIdx.x, re-derived at the use instead of kept in a register)
-#define qpos (p.q_pos0 + ld_shared_s32(smem_addr(&bars->row_t[0][0]) + 4u * (SPLIT == 1 ? threadIdx.x : tt * BM + r)))
+#define t_row (ld_shared_s32(smem_addr(&bars->row_t[0][0]) + 4u * (SPLIT == 1 ? threadIdx.x : tt * BM + r)))
+#define qpos (p.q_pos0 + t_row)
         const int nkt = tt == 0 ? n_kt0 : n_kt1;
         const int t_lo = (row0 + tt * BM) / g;
         const int t_hi_tile = min(p.n_q - 1, (row0 + tt * BM + BM - 1) / g);
@@ -688,7 +704,138 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     m_run = mref;
                     continue;
                 }
-                if constexpr (SPLIT_S && SPLIT == 1) {
+                if constexpr (SPLIT_S && SPLIT == 1 && SUMCHECK) {
+#ifdef HI_FAKE_SOFTMAX  // timing experiment only: the pipeline without the softmax math (P = raw S bits)
+                    tc_fence_before();
+                    mbar_arrive(bar_pl(tt));
+                    mbar_arrive(bar_p(tt));
+                    continue;
+#endif
+                    // Sum-checked lazy rescale.  The max-first rule moves the reference m only when the tile's row
+                    // max exceeds it by more than 2^8, so when it does not, every p = 2^(s*scale - m_run) <= 2^8.
+                    // Conversely a half whose sum of p is <= 2^8 has every p <= 2^8 (p >= 0): then the reference
+                    // stays, exactly as the max-first path would decide, and the half's max is never needed.  So on
+                    // unmasked tiles with a finite reference the softmax exponentiates each half against m_run
+                    // straight away and checks its sum; only a half whose sum exceeds 2^8 takes its max:
+                    //   first half (P not released yet): the raw scores the packing overwrote are re-read from TMEM
+                    //     (S is intact) and the tile takes the max-first path;
+                    //   second half (P_lo released, PV(j)_lo accumulating at m_run): its max comes from the raw
+                    //     scores still in registers; if the reference must move, the warp waits for PV(j)_lo,
+                    //     rescales O (and the running sum) by 2^(m_run - m_new) and redoes the half.
+                    // Masked tiles (causal diagonal, segment tail, duo band edge) and the first tile keep max-first.
+                    constexpr float THR = 256.f;  // 2^RESCALE_THRESHOLD
+                    f2 acc[4];
+                    const f2 sc2{sc, sc};
+                    f2 nm2{-m_run, -m_run};
+                    auto exp_keys = [&](auto lo_c, auto hi_c) {  // keys [LO, HI) -> packed pairs x[i/2]; sum in acc
+                        constexpr int LO = decltype(lo_c)::value, HI = decltype(hi_c)::value;
+                        acc[0] = acc[1] = acc[2] = acc[3] = f2{0.f, 0.f};
+#pragma unroll
+                        for (int i = LO; i < HI; i += 2) {
+                            const f2 a = ffma2(f2{__uint_as_float(x[i]), __uint_as_float(x[i + 1])}, sc2, nm2);
+                            const f2 pp = poly_pair(i >> 1) ? ex2_poly2(a) : f2{ex2(a.x), ex2(a.y)};
+                            acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], pp);
+                            x[i / 2] = pack_bf16(pp.x, pp.y);
+                        }
+                        const f2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+                        return (s01.x + s01.y) + (s23.x + s23.y);
+                    };
+                    auto o_rescale = [&](float a) {  // O *= a (this thread's row)
+#pragma unroll
+                        for (int cb = 0; cb < HD / 32; ++cb) {
+                            uint32_t v[32];
+                            tmem_ld32(t_o + cb * 32, v);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * a);
+                            tmem_st32(t_o + cb * 32, v);
+                        }
+                    };
+                    const bool band_edge = band && p.k_pos0 + kt0 <= p.q_pos0 + t_hi_tile - p.win;
+                    bool fast = !need_mask && !band_edge && __all_sync(0xffffffffu, m_run != -CUDART_INF_F);
+                    float mref = m_run, l_part = 0.f;
+                    // ---- keys [0, KS): max-first, or sum-checked against m_run (a failed check retries max-first)
+#pragma unroll 1
+                    for (int pass = 0; pass < 2; ++pass) {
+                        float alp = 1.f;
+                        if (!fast) {
+                            float mk[8];
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) mk[c] = __uint_as_float(x[c]);
+#pragma unroll
+                            for (int i = 8; i < HN; i += 8)
+#pragma unroll
+                                for (int c = 0; c < 8; ++c) mk[c] = fmaxf(mk[c], __uint_as_float(x[i + c]));
+#ifdef HI_FAKE_MAX  // timing experiment only (wrong results): the row max of 8 scores instead of 128
+                            const float mx = fmaxf(fmaxf(fmaxf(__uint_as_float(x[0]), __uint_as_float(x[1])), fmaxf(__uint_as_float(x[2]), __uint_as_float(x[3]))),
+                                                   fmaxf(fmaxf(__uint_as_float(x[4]), __uint_as_float(x[5])), fmaxf(__uint_as_float(x[6]), __uint_as_float(x[7]))));
+#else
+                            const float mx = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])), fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7])));
+#endif
+                            const float mxs = mx * sc;
+                            const bool grw = (mx != -CUDART_INF_F) && (m_run == -CUDART_INF_F || mxs > m_run + RESCALE_THRESHOLD);
+                            mref = grw ? mxs : m_run;
+                            alp = grw ? ((m_run == -CUDART_INF_F) ? 0.f : ex2(m_run - mxs)) : 1.f;
+                            HI_TR(ttr + 1, j);
+                            // O correction before PV(j)_lo may accumulate (PV(j-1) is complete: S(j) was issued after it)
+                            if ((!first || j > 0) && __any_sync(0xffffffffu, grw)) o_rescale(alp);
+                            const float nm = (mref == -CUDART_INF_F) ? 0.f : -mref;
+                            nm2 = f2{nm, nm};
+                        }
+                        const float s_lo = exp_keys(std::integral_constant<int, 0>{}, std::integral_constant<int, KS>{});
+                        if (fast && __any_sync(0xffffffffu, !(s_lo <= THR))) {
+                            // restore the raw scores of keys [0, KS/2) that the packing overwrote; retry max-first
+                            tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                            tmem_wait_ld();
+                            fast = false;
+                            continue;
+                        }
+                        l_part = l_run * alp + s_lo;
+                        break;
+                    }
+                    tmem_st32(t_s + P_COL, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(bar_pl(tt));  // PV(j)_lo may start
+                    HI_TR(ttr + 2, j);
+                    // ---- keys [KS, 128)
+                    float s_hi = 0.f;
+#pragma unroll 1
+                    for (int pass = 0; pass < 2; ++pass) {
+                        s_hi = exp_keys(std::integral_constant<int, KS>{}, std::integral_constant<int, BN>{});
+                        if (fast && pass == 0 && __any_sync(0xffffffffu, !(s_hi <= THR))) {
+                            float mk[8];  // max of the half's raw scores x[KS..127] (the packing wrote x[KS/2..63])
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) mk[c] = __uint_as_float(x[KS + c]);
+#pragma unroll
+                            for (int i = KS + 8; i < HN; i += 8)
+#pragma unroll
+                                for (int c = 0; c < 8; ++c) mk[c] = fmaxf(mk[c], __uint_as_float(x[i + c]));
+                            const float mxs = fmaxf(fmaxf(fmaxf(mk[0], mk[1]), fmaxf(mk[2], mk[3])),
+                                                    fmaxf(fmaxf(mk[4], mk[5]), fmaxf(mk[6], mk[7]))) * sc;
+                            const bool grw = mxs > m_run + RESCALE_THRESHOLD;
+                            if (__any_sync(0xffffffffu, grw)) {
+                                const float alp2 = grw ? ex2(m_run - mxs) : 1.f;
+                                mref = grw ? mxs : m_run;
+                                mbar_wait(bar_pvl(tt), j & 1);  // O holds PV(j)_lo at the old reference
+                                tc_fence_after();
+                                o_rescale(alp2);
+                                l_part *= alp2;
+                                nm2 = f2{-mref, -mref};
+                                continue;
+                            }
+                        }
+                        break;
+                    }
+                    tmem_st32(t_s + P_COL + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(bar_p(tt));
+                    HI_TR(ttr + 4, j);
+                    l_run = l_part + s_hi;
+                    m_run = mref;
+                    continue;
+                } else if constexpr (SPLIT_S && SPLIT == 1) {
 #ifdef HI_FAKE_SOFTMAX  // timing experiment only: the pipeline without the softmax math (P = raw S bits)
                     tc_fence_before();
                     mbar_arrive(bar_pl(tt));
@@ -976,7 +1123,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (last) {
                 const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
-                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (hq * g + rg % g) * D + hf * HD;
+                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t_row) * p.o_tok_stride + (hq * g + rg % g) * D + hf * HD;
 #pragma unroll
                 for (int cb = 0; cb < HD / 32; ++cb) {
                     uint32_t v[32];
@@ -1024,11 +1171,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     }
 #undef qpos
+#undef t_row
     tc_fence_before();
     __syncthreads();
     if (warp == WARP_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+#undef tmem
     }
 }
 

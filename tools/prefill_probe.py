@@ -65,7 +65,7 @@ def main():
     st1 = hi.stats()
     ms = st1["prefill_attn_ms"] - st0["prefill_attn_ms"]
     fl = st1["prefill_attn_flops"] - st0["prefill_attn_flops"]
-    res = {"variant": os.environ.get("HI_LIB_VARIANT", "product") + (f"+0x{a.flags:x}" if a.flags else ""), "ctx": S, "group": a.group, "layers": L,
+    res = {"variant": os.environ.get("HI_LIB_VARIANT", "product") + (f"+0x{a.flags:x}" if a.flags else ""), "ctx": S, "group": a.group, "layers": L, "dist": a.dist,
            "resident": a.resident, "slot_tokens": hi.stats()["slot_tokens"],
            "steps": steps, "kernel_tflops": round(fl / ms / 1e9, 1), "kernel_ms_per_step": round(ms / steps, 2),
            "launches_per_step": (st1["prefill_attn_launches"] - st0["prefill_attn_launches"]) / steps,
