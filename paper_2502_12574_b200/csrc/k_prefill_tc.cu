@@ -339,9 +339,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    // the TMEM base is re-read from shared memory where each role needs it (one copy live across the role split
-    // spilled to local memory)
+#if HI_SUMCHECK
+    // the TMEM base is re-read from shared memory where each role needs it (with the sum-checked softmax, one copy
+    // live across the role split spills to local memory)
 #define tmem static_cast<uint32_t>(ld_shared_s32(smem_addr(&bars->tmem_base)))
+#else
+    const uint32_t tmem = bars->tmem_base;
+#endif
 
     if (warp >= SOFTMAX_WARPS) {
         setmaxnreg_producer<D>();
@@ -1123,7 +1127,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (last) {
                 const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+#if HI_SUMCHECK
                 __nv_bfloat16* dst = p.out + static_cast<int64_t>(t_row) * p.o_tok_stride + (hq * g + rg % g) * D + hf * HD;
+#else
+                __nv_bfloat16* dst = p.out + static_cast<int64_t>(t) * p.o_tok_stride + (hq * g + rg % g) * D + hf * HD;
+#endif
 #pragma unroll
                 for (int cb = 0; cb < HD / 32; ++cb) {
                     uint32_t v[32];
@@ -1177,7 +1185,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp == WARP_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+#if HI_SUMCHECK
 #undef tmem
+#endif
     }
 }
 
