@@ -195,6 +195,179 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------- CTA-pair GEMM (cta_group::2)
+// gemm_tc2_kernel: a cluster of two CTAs computes 256 (tokens) x 256 (out features) tiles with
+// tcgen05.mma.cta_group::2 M256 N256 K16: each CTA loads its own 128 activation rows and HALF of the 256 weight
+// rows of every K step (the MMA reads the other half from the peer's shared memory at the same offset) and keeps
+// its 128 x 256 fp32 accumulator rows in its own TMEM.  Per SM and K step that is 32 KiB of TMA and 32 KiB of
+// operand reads instead of 48 + 48 KiB with a 128 x 256 tile per CTA: the shared-memory port, not the tensor
+// pipe, bounded the single-CTA kernel.  The leader CTA's MMA warp issues for the pair; both CTAs' TMA bytes land
+// on the leader's full[] barriers; commits are multicast to both CTAs (empty[], acc_full[]); both CTAs'
+// epilogue warps release an accumulator buffer on the leader's acc_empty[].
+#ifndef HI_GEMM_2CTA
+#define HI_GEMM_2CTA 1
+#endif
+constexpr int P_GM = 256, P_GN = 256, P_GK = 64;    // pair tile; per CTA 128 rows of X, 128 rows of W per K step
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * P_GK * 2;           // 16 KiB: this CTA's activation rows
+constexpr int P_B_BYTES = 128 * P_GK * 2;           // 16 KiB: this CTA's half of the weight rows
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+struct __align__(8) PairBars {
+    uint64_t full[P_STAGES], empty[P_STAGES];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem_base;
+};
+constexpr int P_SMEM = P_STAGES * P_STAGE_BYTES + static_cast<int>(sizeof(PairBars)) + 1024;
+
+template <bool F32OUT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                    void* __restrict__ yv, int n, int mo, int kd, int beta) {
+    extern __shared__ uint8_t g_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(g_raw) + 1023) & ~uintptr_t(1023));
+    PairBars* bars = reinterpret_cast<PairBars*>(smem + P_STAGES * P_STAGE_BYTES);
+    const uint32_t sbase = smem_addr(smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int tiles_m = (n + P_GM - 1) / P_GM, tiles_n = (mo + P_GN - 1) / P_GN, tiles = tiles_m * tiles_n;
+    const int kt = (kd + P_GK - 1) / P_GK;
+    auto full = [&](int s) { return smem_addr(&bars->full[s]); };
+    auto empty = [&](int s) { return smem_addr(&bars->empty[s]); };
+    auto accf = [&](int b) { return smem_addr(&bars->acc_full[b]); };
+    auto acce = [&](int b) { return smem_addr(&bars->acc_empty[b]); };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < P_STAGES; ++s) {
+            mbar_init(full(s), 1);    // leader's: its producer's arrive.expect_tx; both CTAs' bytes
+            mbar_init(empty(s), 1);   // both: one multicast commit per use
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(accf(b), 1);                  // both: one multicast commit per tile
+            mbar_init(acce(b), 2 * G_EPI_WARPS);    // leader's: every epilogue warp of the pair
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&bars->tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();   // both CTAs' barriers initialised and TMEM allocated before any cross-CTA traffic
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---------------- TMA producer (both CTAs): this CTA's X rows and half of the W rows
+            int it = 0;
+            for (int t = pair; t < tiles; t += n_pairs) {
+                int mb, nb;
+                tile_coords(t, tiles_m, tiles_n, mb, nb);
+                for (int k = 0; k < kt; ++k, ++it) {
+                    const int s = it % P_STAGES;
+                    if (it >= P_STAGES) mbar_wait_cluster(empty(s), ((it / P_STAGES) - 1) & 1);
+                    if (leader) mbar_expect_tx(full(s), 2 * P_STAGE_BYTES);   // OOB rows are zero-filled, still counted
+                    const uint32_t full_l = mapa_shared(full(s), 0);
+                    tma_load_2d_cg2(sbase + s * P_STAGE_BYTES, &tm_x, full_l, k * P_GK, mb * P_GM + static_cast<int>(rank) * 128);
+                    tma_load_2d_cg2(sbase + s * P_STAGE_BYTES + P_A_BYTES, &tm_w, full_l, k * P_GK,
+                                    nb * P_GN + static_cast<int>(rank) * 128);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {   // ---------------- MMA issuer for the pair: the whole warp runs the loop, elect.sync issues
+            constexpr uint32_t IDESC = idesc_bf16(P_GM, P_GN, false);
+            int it = 0, i = 0;
+            for (int t = pair; t < tiles; t += n_pairs, ++i) {
+                const int b = i & 1;
+                if (i >= 2) mbar_wait_cluster(acce(b), ((i >> 1) - 1) & 1);   // both epilogues drained this buffer
+                tc_fence_after();
+                const uint32_t acc = tmem + b * P_GN;
+                for (int k = 0; k < kt; ++k, ++it) {
+                    const int s = it % P_STAGES;
+                    mbar_wait_cluster(full(s), (it / P_STAGES) & 1);
+                    tc_fence_after();
+                    const uint64_t da = sdesc(sbase + s * P_STAGE_BYTES, 16, 1024);
+                    const uint64_t db = sdesc(sbase + s * P_STAGE_BYTES + P_A_BYTES, 16, 1024);
+#pragma unroll
+                    for (int kk = 0; kk < P_GK / 16; ++kk)
+                        umma_bf16_cg2_w(acc, da + (kk * 2), db + (kk * 2), IDESC, (k > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit_cg2_mc_w(empty(s), 0x3);   // both CTAs' stage s is free once these MMAs have read it
+                }
+                umma_commit_cg2_mc_w(accf(b), 0x3);        // both CTAs' accumulator rows complete
+            }
+        }
+    } else {
+        // ---------------- epilogue (both CTAs): warp w owns TMEM lanes 32*(w%4) .. +31 = rows of this CTA's half
+        const int q = warp & 3;
+        const int r_in = static_cast<int>(rank) * 128 + q * 32 + lane;
+        const uint32_t acce_l0 = mapa_shared(acce(0), 0), acce_l1 = mapa_shared(acce(1), 0);
+        int i = 0;
+        for (int t = pair; t < tiles; t += n_pairs, ++i) {
+            int mb, nb;
+            tile_coords(t, tiles_m, tiles_n, mb, nb);
+            const int b = i & 1;
+            mbar_wait_cluster(accf(b), (i >> 1) & 1);
+            tc_fence_after();
+            const int row = mb * P_GM + r_in;
+            const bool live = row < n;
+            const int64_t yoff = static_cast<int64_t>(row) * mo + nb * P_GN;
+            const uint32_t taddr = tmem + b * P_GN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < P_GN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(taddr + c * 32, v);
+                tmem_wait_ld();
+                const int col = nb * P_GN + c * 32;
+                if (F32OUT && live && col < mo) {
+                    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(yv) + yoff + c * 32);
+#pragma unroll
+                    for (int e4 = 0; e4 < 8; ++e4)
+                        dst[e4] = make_float4(__uint_as_float(v[4 * e4]), __uint_as_float(v[4 * e4 + 1]),
+                                              __uint_as_float(v[4 * e4 + 2]), __uint_as_float(v[4 * e4 + 3]));
+                } else if (live && col < mo) {
+                    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(yv) + yoff + c * 32);
+                    float f[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(v[e]);
+                    if (beta) {
+#pragma unroll
+                        for (int e8 = 0; e8 < 4; ++e8) {
+                            const uint4 u = dst[e8];
+                            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                f[e8 * 8 + 2 * h] += __uint_as_float(w4[h] << 16);
+                                f[e8 * 8 + 2 * h + 1] += __uint_as_float(w4[h] & 0xffff0000u);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int e8 = 0; e8 < 4; ++e8) {
+                        uint4 o;
+                        o.x = pack_bf16(f[e8 * 8 + 0], f[e8 * 8 + 1]);
+                        o.y = pack_bf16(f[e8 * 8 + 2], f[e8 * 8 + 3]);
+                        o.z = pack_bf16(f[e8 * 8 + 4], f[e8 * 8 + 5]);
+                        o.w = pack_bf16(f[e8 * 8 + 6], f[e8 * 8 + 7]);
+                        dst[e8] = o;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(b ? acce_l1 : acce_l0);   // this warp's rows of the buffer are drained
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();   // the pair's last MMAs wrote both CTAs' TMEM; free it only when both are done
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 // y[o] = (beta ? y[o] : 0) + x . W[o, :]; 8 warps per CTA, 2 output rows per warp, x staged in shared memory
 constexpr int GV_WARPS = 8, GV_ROWS = 2;
 
@@ -255,6 +428,23 @@ cudaError_t launch_gemm_t(const __nv_bfloat16* w, const __nv_bfloat16* x, void* 
         gemv_kernel<F32OUT><<<(mo + rows_per_cta - 1) / rows_per_cta, GV_WARPS * 32, smem, stream>>>(w, x, y, mo, kd, beta);
         return cudaGetLastError();
     }
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (HI_GEMM_2CTA) {
+        static std::atomic<unsigned long long> configured2{0};
+        if (cudaError_t e = set_smem_attr_once(gemm_tc2_kernel<F32OUT>, P_SMEM, configured2); e != cudaSuccess) return e;
+        CUtensorMap tx, tw;
+        const cuuint64_t dx[2] = {static_cast<cuuint64_t>(kd), static_cast<cuuint64_t>(n)};
+        const cuuint64_t dw[2] = {static_cast<cuuint64_t>(kd), static_cast<cuuint64_t>(mo)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(kd) * 2};
+        const cuuint32_t box[2] = {P_GK, 128};
+        if (!make_tmap_bf16(&tx, x, 2, dx, strides, box)) return cudaErrorInvalidValue;
+        if (!make_tmap_bf16(&tw, w, 2, dw, strides, box)) return cudaErrorInvalidValue;
+        const int tiles = ((n + P_GM - 1) / P_GM) * ((mo + P_GN - 1) / P_GN);
+        const int pairs = tiles < sms / 2 ? tiles : sms / 2;
+        gemm_tc2_kernel<F32OUT><<<2 * pairs, G_THREADS, P_SMEM, stream>>>(tx, tw, y, n, mo, kd, beta);
+        return cudaGetLastError();
+    }
     static std::atomic<unsigned long long> configured{0};
     if (cudaError_t e = set_smem_attr_once(gemm_tc_kernel<F32OUT>, G_SMEM, configured); e != cudaSuccess) return e;
     CUtensorMap tx, tw;
@@ -270,8 +460,6 @@ cudaError_t launch_gemm_t(const __nv_bfloat16* w, const __nv_bfloat16* x, void* 
         const cuuint32_t box[2] = {GK, GN};
         if (!make_tmap_bf16(&tw, w, 2, dims, strides, box)) return cudaErrorInvalidValue;
     }
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = ((n + GM - 1) / GM) * ((mo + GN - 1) / GN);
     gemm_tc_kernel<F32OUT><<<tiles < sms ? tiles : sms, G_THREADS, G_SMEM, stream>>>(tx, tw, y, n, mo, kd, beta);
     return cudaGetLastError();
