@@ -38,6 +38,7 @@ def _check(n, mo, kd, beta, seed=0):
     (300, 640, 200, True),       # M, N and K tails, residual
     (2, 64, 8, False),           # the smallest GEMM (tails everywhere)
     (2048, 4096, 64, True),      # 256 tiles on 148 CTAs: the persistent loop and both TMEM accumulators
+    (4096, 8192, 128, True),     # ~7 pair tiles per CTA pair: each accumulator buffer drained and re-filled 3+ times
     (1024, 6144, 4096, False),   # Llama-3-8B QKV at a 1024-token chunk
     (1024, 4096, 4096, True),    # O projection + residual
     (517, 4096, 14336, True),    # down projection + residual, ragged chunk
