@@ -116,8 +116,13 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #ifndef HI_WAIT_HINT_MMA
 #define HI_WAIT_HINT_MMA 0
 #endif
+#ifndef HI_MMA_SPIN
+#define HI_MMA_SPIN 0   // A/B: the MMA warp polls with the non-blocking test_wait instead of try_wait
+#endif
 #if HI_WAIT_HINT_MMA
 #define MMA_WAIT(bar, par) mbar_wait_hint(bar, par, HI_WAIT_HINT_MMA)
+#elif HI_MMA_SPIN
+#define MMA_WAIT(bar, par) do { while (!mbar_test(bar, par)) { } } while (0)
 #else
 #define MMA_WAIT(bar, par) mbar_wait(bar, par)
 #endif
