@@ -199,6 +199,13 @@ constexpr int P_COL = SPLIT_S_LO ? 64 : 0;    // first packed P column
 #define HI_P_SPLIT_KEYS 64
 #endif
 constexpr int KS = HI_P_SPLIT_KEYS;
+// HI_P_PARTS=4 (A/B): P released in four 32-key quarters (PV(j) issued in four parts; only the last 32 keys' PV
+// stays on the chain) instead of two halves
+#ifndef HI_P_PARTS
+#define HI_P_PARTS 2
+#endif
+constexpr int P_PARTS = HI_P_PARTS;
+static_assert(P_PARTS == 2 || (P_PARTS == 4 && KS == 64 && HI_SPLIT_S == 2 && SPLIT == 1), "quarters: product split only");
 constexpr bool SUMCHECK = HI_SUMCHECK != 0 && HI_SPLIT_S == 2 && !HI_PINGPONG && !HI_SPEC_SPLIT && HI_P_SPLIT_KEYS == 64;
 static_assert(KS == 64 || KS == 96, "P split at 64 or 96 keys");
 static_assert(SPLIT == 1 || !SPLIT_S || (KS == 64 && !SPLIT_S_LO), "two warps per row split P at their 64-key boundary");
@@ -213,6 +220,7 @@ struct __align__(8) Barriers {
     uint64_t s_full[2], p_full[2], o_done[2];
     uint64_t s_cons[2], p_lo[2];  // split schedule: S(j) read into registers / P(j) keys 0-63 stored
     uint64_t pv_lo[2];            // SUMCHECK: PV(j)_lo of tile t complete (a second-half rescale waits for it)
+    uint64_t p_q[2][2];           // P_PARTS == 4: P(j) keys 32..63 / 64..95 stored (quarter 0 = p_lo, 3 = p_full)
     uint64_t tok[2][4];           // PINGPONG: MUFU token for tile t's warp on SMSP q (arrived by the other tile)
     uint32_t tmem_base;
     volatile int tile_done[2];    // PINGPONG: tile t has taken its last turn (its partner stops waiting for it)
@@ -311,6 +319,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto bar_sc = [&](int t) { return smem_addr(&bars->s_cons[t]); };
     auto bar_pl = [&](int t) { return smem_addr(&bars->p_lo[t]); };
     auto bar_pvl = [&](int t) { return smem_addr(&bars->pv_lo[t]); };
+    auto bar_pq = [&](int t, int q) { return smem_addr(&bars->p_q[t][q]); };
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
@@ -329,6 +338,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(bar_sc(t), 128);
             mbar_init(bar_pl(t), 128 * SPLIT);
             mbar_init(bar_pvl(t), 1);
+            mbar_init(bar_pq(t, 0), 128);
+            mbar_init(bar_pq(t, 1), 128);
             for (int q = 0; q < 4; ++q) mbar_init(smem_addr(&bars->tok[t][q]), 1);
         }
         // a tile without KV tiles never takes a turn (its partner must not wait for it)
@@ -438,6 +449,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         HI_UMMA(tmem_m + tt * 256 + 64 * h, a0 + off, b0 + off, ID_S64, ks > 0);
                     }
                 };
+                // O_tt += P_tt(j)[keys 16 kk0 .. 16 kk1) V(j)[same keys]
+                auto issue_pv_range = [&](int tt, int j, int kk0, int kk1) {
+                    const uint64_t b0 = dv0 + (((j % NS) * (D / 64) * L::BOX) >> 4);
+                    for (int kk = kk0; kk < kk1; ++kk)
+                        HI_UMMA_TS(tmem_m + tt * 256 + 128, tmem_m + tt * 256 + P_COL + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
+                                   (j > 0 || kk > 0 || !first) ? 1u : 0u);
+                };
+                (void)issue_pv_range;
                 // O_tt += P_tt(j)[keys 64h ..] V(j)[keys 64h ..]; P at packed columns 64 + 32h ..
                 auto issue_pv_half = [&](int tt, int j, int h) {
                     const uint64_t b0 = dv0 + (((j % NS) * (D / 64) * L::BOX) >> 4);
@@ -466,12 +485,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         MMA_WAIT(bar_pl(tt), j & 1);
                         if (!waited_v) { MMA_WAIT(bar_v(s), (j / NS) & 1); waited_v = true; }
                         tc_fence_after();
+                        if constexpr (P_PARTS == 4) {
+                            issue_pv_range(tt, j, 0, 2);
+                            MMA_WAIT(bar_pq(tt, 0), j & 1);
+                            tc_fence_after();
+                            issue_pv_range(tt, j, 2, 4);
+                            MMA_WAIT(bar_pq(tt, 1), j & 1);
+                            tc_fence_after();
+                            issue_pv_range(tt, j, 4, 6);
+                            MMA_WAIT(bar_p(tt), j & 1);
+                            HI_TR_MMA(12 + 2 * tt, j);
+                            tc_fence_after();
+                            issue_pv_range(tt, j, 6, 8);
+                        } else {
                         issue_pv_half(tt, j, 0);
                         if constexpr (SUMCHECK) HI_UCOMMIT(bar_pvl(tt));  // PV(j)_lo done (a rare second-half rescale)
                         MMA_WAIT(bar_p(tt), j & 1);
                         HI_TR_MMA(12 + 2 * tt, j);
                         tc_fence_after();
                         issue_pv_half(tt, j, 1);
+                        }
                         if (j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));
                         if (tt == last_v_tile(j)) HI_UCOMMIT(bar_ve(s));  // V(j) consumed by every tile
                         if (next) {
@@ -966,6 +999,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if (pp && (tt == 1 || j > 0) && !bars->tile_done[tt ^ 1]) {
                         // my turn: tile 0 before KV tile j waits for tile 1's turn j-1, tile 1 for tile 0's turn j
                         mbar_wait(smem_addr(&bars->tok[tt][wq]), tt == 0 ? ((j - 1) & 1) : (j & 1));
+                    }
+                    if constexpr (P_PARTS == 4) {
+                        // quarter q: keys [32 q, 32 q + 32) -> packed columns [P_COL + 16 q, + 16), released on
+                        // p_lo / p_q[0] / p_q[1] / p_full
+                        exp_keys(std::integral_constant<int, 0>{}, std::integral_constant<int, 32>{});
+                        tmem_st16(t_s + P_COL, &x[0]);
+                        release_p(bar_pl(tt));
+                        exp_keys(std::integral_constant<int, 32>{}, std::integral_constant<int, 64>{});
+                        tmem_st16(t_s + P_COL + 16, &x[16]);
+                        release_p(bar_pq(tt, 0));
+                        exp_keys(std::integral_constant<int, 64>{}, std::integral_constant<int, 96>{});
+                        tmem_st16(t_s + P_COL + 32, &x[32]);
+                        release_p(bar_pq(tt, 1));
+                        exp_keys(std::integral_constant<int, 96>{}, std::integral_constant<int, 128>{});
+                        tmem_st16(t_s + P_COL + 48, &x[48]);
+                        release_p(bar_p(tt));
+                        HI_TR(ttr + 4, j);
+                        const f2 q01 = fadd2(acc[0], acc[1]), q23 = fadd2(acc[2], acc[3]);
+                        l_run = l_run * alp + ((q01.x + q01.y) + (q23.x + q23.y));
+                        m_run = mref;
+                        continue;
                     }
                     // keys [0, KS) -> packed columns [P_COL, P_COL + KS/2): PV(j)_lo may start
                     if (!spec_ok) exp_keys(std::integral_constant<int, 0>{}, std::integral_constant<int, KS>{});
