@@ -86,7 +86,15 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #ifndef HI_WARP_ISSUE
 #define HI_WARP_ISSUE 1
 #endif
-#if HI_WARP_ISSUE
+// HI_DESC_LO (with HI_WARP_ISSUE): pass only the descriptors' low words (the high word is the constant DESC_HI)
+#ifndef HI_DESC_LO
+#define HI_DESC_LO 1
+#endif
+#if HI_WARP_ISSUE && HI_DESC_LO
+#define HI_UMMA(d, a, b, i, acc) umma_bf16_wl(d, static_cast<uint32_t>(a), static_cast<uint32_t>(b), i, acc)
+#define HI_UMMA_TS(d, a, b, i, acc) umma_bf16_ts_wl(d, a, static_cast<uint32_t>(b), i, acc)
+#define HI_UCOMMIT umma_commit_w
+#elif HI_WARP_ISSUE
 #define HI_UMMA umma_bf16_w
 #define HI_UMMA_TS umma_bf16_ts_w
 #define HI_UCOMMIT umma_commit_w
@@ -406,6 +414,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t dq0 = sdesc(sbase + L::Q_OFF, 16, 1024);
             const uint64_t dk0 = sdesc(sbase + L::K_OFF, 16, 1024);
             const uint64_t dv0 = sdesc(sbase + L::V_OFF, L::BOX, 1024);
+            if (HI_DESC_LO && ((dq0 >> 32) != DESC_HI || (dk0 >> 32) != DESC_HI || (dv0 >> 32) != DESC_HI)) __trap();
             auto issue_s = [&](int tt, int i) {  // S_tt(i) = Q_tt K(i)^T
                 const int s = i % NS;
                 const uint64_t a0 = dq0 + ((tt * (D / 64) * L::BOX) >> 4);
