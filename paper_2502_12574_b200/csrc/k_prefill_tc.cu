@@ -86,9 +86,11 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #ifndef HI_WARP_ISSUE
 #define HI_WARP_ISSUE 1
 #endif
-// HI_DESC_LO (with HI_WARP_ISSUE): pass only the descriptors' low words (the high word is the constant DESC_HI)
+// HI_DESC_LO=1 (A/B, off; with HI_WARP_ISSUE): pass only the descriptors' low words (the high word is the constant
+// DESC_HI): ~13 instead of ~19 issuer instructions per tcgen05.mma, parity-green, but 743 vs 765 TFLOP/s per GHz in
+// the sustained probe (job AO) -- a faster issuer is not a faster kernel here (see also HI_MMA_SPIN)
 #ifndef HI_DESC_LO
-#define HI_DESC_LO 1
+#define HI_DESC_LO 0
 #endif
 #if HI_WARP_ISSUE && HI_DESC_LO
 #define HI_UMMA(d, a, b, i, acc) umma_bf16_wl(d, static_cast<uint32_t>(a), static_cast<uint32_t>(b), i, acc)
@@ -109,6 +111,11 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 // job AH): without the max phase the two tiles' exponential phases collide on the MUFU more often.
 #ifndef HI_SUMCHECK
 #define HI_SUMCHECK 0
+#endif
+// HI_TWO_ISSUERS=1 (A/B): each Q tile's MMAs are issued by its own warp (warp 9: tile 0, warp 10: tile 1), each
+// waiting only on its own tile's barriers (no fixed A-then-B issue order), with per-tile K/V release barriers
+#ifndef HI_TWO_ISSUERS
+#define HI_TWO_ISSUERS 0
 #endif
 // HI_KV_JOINT=1 (A/B only): the producer loads K(i) only once V(i - NS) is released too, in K(i), V(i) order -- the
 // round-1 prefetch distance (one tile step for K) with the separate barriers
@@ -214,6 +221,7 @@ constexpr int KS = HI_P_SPLIT_KEYS;
 #endif
 constexpr int P_PARTS = HI_P_PARTS;
 static_assert(P_PARTS == 2 || (P_PARTS == 4 && KS == 64 && HI_SPLIT_S == 2 && SPLIT == 1), "quarters: product split only");
+static_assert(!HI_TWO_ISSUERS || (HI_SPLIT_S == 2 && !HI_KV_JOINT), "two issuers: the product split schedule only");
 constexpr bool SUMCHECK = HI_SUMCHECK != 0 && HI_SPLIT_S == 2 && !HI_PINGPONG && !HI_SPEC_SPLIT && HI_P_SPLIT_KEYS == 64;
 static_assert(KS == 64 || KS == 96, "P split at 64 or 96 keys");
 static_assert(SPLIT == 1 || !SPLIT_S || (KS == 64 && !SPLIT_S_LO), "two warps per row split P at their 64-key boundary");
@@ -225,6 +233,7 @@ using namespace ptx;
 struct __align__(8) Barriers {
     uint64_t q_full;
     uint64_t k_full[NS], v_full[NS], k_empty[NS], v_empty[NS];  // K and V stages are released separately
+    uint64_t k_empty2[2][NS], v_empty2[2][NS];                      // HI_TWO_ISSUERS: released per tile
     uint64_t s_full[2], p_full[2], o_done[2];
     uint64_t s_cons[2], p_lo[2];  // split schedule: S(j) read into registers / P(j) keys 0-63 stored
     uint64_t pv_lo[2];            // SUMCHECK: PV(j)_lo of tile t complete (a second-half rescale waits for it)
@@ -321,6 +330,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto bar_v = [&](int s) { return smem_addr(&bars->v_full[s]); };
     auto bar_ke = [&](int s) { return smem_addr(&bars->k_empty[s]); };
     auto bar_ve = [&](int s) { return smem_addr(&bars->v_empty[s]); };
+    auto bar_ke2 = [&](int t, int s) { return smem_addr(&bars->k_empty2[t][s]); };
+    auto bar_ve2 = [&](int t, int s) { return smem_addr(&bars->v_empty2[t][s]); };
     auto bar_s = [&](int t) { return smem_addr(&bars->s_full[t]); };
     auto bar_p = [&](int t) { return smem_addr(&bars->p_full[t]); };
     auto bar_o = [&](int t) { return smem_addr(&bars->o_done[t]); };
@@ -336,6 +347,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(bar_v(s), 1);
             mbar_init(bar_ke(s), 1);
             mbar_init(bar_ve(s), 1);
+            mbar_init(bar_ke2(0, s), 1);
+            mbar_init(bar_ke2(1, s), 1);
+            mbar_init(bar_ve2(0, s), 1);
+            mbar_init(bar_ve2(1, s), 1);
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(bar_s(t), 1);
@@ -386,7 +401,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // K(0), then K(i+1) ahead of V(i).
             auto load_k = [&](int i) {
                 const int s = i % NS;
-                if (i >= NS) mbar_wait(bar_ke(s), ((i / NS) - 1) & 1);
+                if (HI_TWO_ISSUERS && i >= NS) {  // every tile that read K(i - NS) released it
+                    for (int t = 0; t < n_tiles; ++t)
+                        if ((t == 0 ? n_kt0 : n_kt1) > i - NS) mbar_wait(bar_ke2(t, s), ((i / NS) - 1) & 1);
+                } else if (i >= NS) {
+                    mbar_wait(bar_ke(s), ((i / NS) - 1) & 1);
+                }
                 if (HI_KV_JOINT && i >= NS) mbar_wait(bar_ve(s), ((i / NS) - 1) & 1);  // A/B: the round-1 joint release
                 mbar_expect_tx(bar_k(s), (D / 64) * L::BOX);
                 for (int c = 0; c < D / 64; ++c)
@@ -397,12 +417,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (HI_KV_JOINT) load_k(i);
                 else if (i + 1 < n_kt) load_k(i + 1);
                 const int s = i % NS;
-                if (i >= NS) mbar_wait(bar_ve(s), ((i / NS) - 1) & 1);
+                if (HI_TWO_ISSUERS && i >= NS) {
+                    for (int t = 0; t < n_tiles; ++t)
+                        if ((t == 0 ? n_kt0 : n_kt1) > i - NS) mbar_wait(bar_ve2(t, s), ((i / NS) - 1) & 1);
+                } else if (i >= NS) {
+                    mbar_wait(bar_ve(s), ((i / NS) - 1) & 1);
+                }
                 mbar_expect_tx(bar_v(s), (D / 64) * L::BOX);
                 for (int c = 0; c < D / 64; ++c)
                     tma_load_3d(sbase + L::V_OFF + (s * (D / 64) + c) * L::BOX, &tm_v, bar_v(s), c * 64, kb + i * BN, hk);
             }
-        } else if (warp == WARP_MMA && (HI_WARP_ISSUE || lane == 0) && n_kt > 0) {
+        } else if ((warp == WARP_MMA || (HI_TWO_ISSUERS && warp == WARP_MMA + 1 && n_tiles == 2)) && (HI_WARP_ISSUE || lane == 0) &&
+                   n_kt > 0) {
             // ============================ MMA issuer ==============================
             const uint32_t tmem_m = tmem;  // read once: the issue loop must not wait on shared memory
             constexpr uint32_t ID_S = idesc_bf16(BM, BN, false);
@@ -439,11 +465,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
                 if (j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));  // O final: the epilogue's only wait
             };
+            // HI_TWO_ISSUERS: this warp's tile; otherwise every tile
+            const int tt_lo = HI_TWO_ISSUERS ? warp - WARP_MMA : 0;
+            const int tt_hi = HI_TWO_ISSUERS ? tt_lo + 1 : n_tiles;
+            const int j_end = HI_TWO_ISSUERS ? nk_t[tt_lo] : n_kt;
             MMA_WAIT(bar_k(0), 0);
             tc_fence_after();
-            for (int tt = 0; tt < n_tiles; ++tt)
+            for (int tt = tt_lo; tt < tt_hi; ++tt)
                 if (nk_t[tt] > 0) issue_s(tt, 0);
-            HI_UCOMMIT(bar_ke(0));  // K(0) consumed once S(0) of every tile is done
+            if (HI_TWO_ISSUERS) {
+                if (j_end > 0) HI_UCOMMIT(bar_ke2(tt_lo, 0));
+            } else {
+                HI_UCOMMIT(bar_ke(0));  // K(0) consumed once S(0) of every tile is done
+            }
             // the last tile that reads V(j) (tiles run to nk_t[tt] key tiles; tile 1's rows are the later ones)
             auto last_v_tile = [&](int j) { return (n_tiles == 2 && j < nk_t[1]) ? 1 : 0; };
             if constexpr (SPLIT_S) {
@@ -474,10 +508,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         HI_UMMA_TS(tmem_m + tt * 256 + 128, tmem_m + tt * 256 + P_COL + kk * 8, b0 + ((kk * 16 * 128) >> 4), ID_O,
                                      (j > 0 || kk > 0 || !first) ? 1u : 0u);
                 };
-                for (int j = 0; j < n_kt; ++j) {
+                for (int j = 0; j < j_end; ++j) {
                     const int s = j % NS;
                     bool waited_v = false, have_k = false;
-                    for (int tt = 0; tt < n_tiles; ++tt) {
+                    for (int tt = tt_lo; tt < tt_hi; ++tt) {
                         if (j >= nk_t[tt]) continue;
                         const bool next = j + 1 < nk_t[tt];
                         bool lo_done = false;
@@ -515,7 +549,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         issue_pv_half(tt, j, 1);
                         }
                         if (j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));
-                        if (tt == last_v_tile(j)) HI_UCOMMIT(bar_ve(s));  // V(j) consumed by every tile
+                        if (HI_TWO_ISSUERS) HI_UCOMMIT(bar_ve2(tt, s));  // this tile is done with V(j)
+                        else if (tt == last_v_tile(j)) HI_UCOMMIT(bar_ve(s));  // V(j) consumed by every tile
                         if (next) {
                             if (!have_k) { MMA_WAIT(bar_k((j + 1) % NS), ((j + 1) / NS) & 1); have_k = true; }
                             tc_fence_after();
@@ -527,9 +562,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 issue_s(tt, j + 1);  // commits s_full
                             }
                             HI_TR_MMA(12 + 2 * tt + 1, j);
+                            if (HI_TWO_ISSUERS) HI_UCOMMIT(bar_ke2(tt, (j + 1) % NS));  // this tile is done with K(j+1)
                         }
                     }
-                    if (j + 1 < n_kt) HI_UCOMMIT(bar_ke((j + 1) % NS));  // K(j+1) consumed by every tile's S(j+1)
+                    if (!HI_TWO_ISSUERS && j + 1 < n_kt) HI_UCOMMIT(bar_ke((j + 1) % NS));  // K(j+1) consumed by every tile's S(j+1)
                 }
             } else {
             for (int j = 0; j < n_kt; ++j) {
