@@ -913,7 +913,8 @@ def sharded_parity(gathered0, gdec, p_last, S, L, hq, hkv, d, world, rank, pg, t
 # ---------------------------------------------------------------------------------------------
 def run_reference(args, rank, world):
     """--impl reference: the fp64 oracle (as it stands) on this box's host cores, same metric/config.
-    Each step is a bounded sample of the workload: rows of the timed chunk (the last chunk before S)."""
+    Each step is a bounded sample of the workload: rows of the ours arm's timed chunk (the mean-history chunk at
+    (S - c)/2, whose per-token work is the whole prefill's average)."""
     if rank != 0:
         return None
     import numpy as np
@@ -925,7 +926,7 @@ def run_reference(args, rank, world):
     wl = args.workload if args.workload != "auto" else "8B-1M"
     L, hq, hkv, d, S, c = WORKLOADS[wl]
     g = hq // hkv
-    pos = S - c
+    pos = (S - c) // 2   # the ours arm's timed chunk (p_t in run())
     if torch.cuda.is_available():
         k, v = _oracle_kv(0, 0, pos + c, d, torch)
     else:
@@ -953,7 +954,7 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (same generator and workload as the ours arm)",
             "config": {"workload": wl, "layers": L, "q_heads": hq, "kv_heads": hkv, "head_dim": d, "context": S,
-                       "chunk": c, "timed_chunk": [pos, S], "parallelism": "host cores"},
+                       "chunk": c, "timed_chunk": [pos, pos + c], "parallelism": "host cores"},
             "cpu_baseline": {"value": round(val, 6), "unit": "tok/s", "cores": cores, "kind": "oracle",
                              "sample": f"per step {rows_per_step} (layer 0, q head, position) rows of the chunk at "
                                        f"{pos}; tok/s = rows/s / ({L} x {hq})"},
