@@ -23,6 +23,25 @@
 // tiles, so one tile's softmax overlaps the other tile's QK^T / PV on the tensor core.
 // Online softmax in the log2 domain with lazy rescaling (the O correction is applied only when a
 // row max grows by more than 2^8), which is exact: O/l does not depend on the reference max.
+//
+// Compile-time switches.  The product build uses the defaults; every other setting is an A/B experiment built only
+// through build.build_variant (-D...), kept with its measurement so the choice stays checkable
+// (profiles/prefill_probe_r02.jsonl; TFLOP/s per GHz in the sustained 1M probe, product ~760):
+//   HI_WARP_ISSUE=1      whole-warp MMA issue, elect.sync per MMA          (lane-0 issue: -10.7 % per clock)
+//   HI_SPLIT_S=2         P released in two halves, PV(j)_lo early           (=0 one piece 679; =1 S_lo early 731)
+//   HI_P_SPLIT_KEYS=64   split point                                         (96: -0.3 %)
+//   HI_P_PARTS=2         halves                                              (4 quarters: 742)
+//   HI_KV_JOINT=0        K and V stages released separately                  (joint: -1.8 %, fake-softmax -8 %)
+//   HI_SOFTMAX_SPLIT=1   one softmax warp per row quarter and tile           (2: spills, 0.85-0.9x in round 1)
+//   HI_SUMCHECK=0        max-first lazy rescale                              (sum-checked: 668)
+//   HI_PINGPONG=0        free-running exponential phases                     (MUFU token ping-pong: 670)
+//   HI_POLY_MASK8/PAIRS  all exponentials on MUFU                             (1/8 on the FMA pipe: +0.8 %/clk, -clock)
+//   HI_SPEC_EXP/SPLIT=0  max before the exponentials                          (speculative first half: -3 %)
+//   HI_TWO_ISSUERS=0     one MMA issuer warp                                 (one per tile: 523)
+//   HI_DESC_LO=0         64-bit descriptors                                  (low words: 743)
+//   HI_MMA_SPIN=0, HI_WAIT_HINT(_MMA)=0: try_wait without a suspend hint     (polling: 711; 2 us hint on the MMA warp: -5 %)
+//   HI_FAKE_SOFTMAX / HI_FAKE_MAX / HI_SKIP_S / HI_SKIP_PV: timing-only (wrong results), never in the product
+//   HI_TRACE: CTA-0 clock64() timeline (hi_debug_prefill_trace), tools/trace_prefill.py
 #include "hi_kernels.cuh"
 #include "tc_ptx.cuh"
 
