@@ -11,7 +11,8 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2502_12574_b200", "libheadinfer.so")
-PRODUCT = ("prefill_tc_kernel", "decode_partial_kernel", "decode_combine_kernel", "pack_kv_kernel")
+PRODUCT = ("prefill_tc_kernel", "decode_partial_kernel", "decode_combine_kernel", "pack_kv_kernel", "gemm_tc2_kernel",
+           "gemv_kernel")
 
 
 def _res_usage():
