@@ -5,7 +5,9 @@
 // (include/hilayer.h; reading R19: the residual add is the epilogue, so x + a W^T is
 // rounded once.)  X is the activation (row-major = K-major), W a PyTorch Linear weight [out, in] (K-major).
 //
-// gemm_tc_kernel (n >= 2): persistent, warp-specialised, one CTA per SM.  Tile 128 (tokens) x 256 (out features)
+// gemm_tc2_kernel (n >= 2, the product; HI_GEMM_2CTA): CTA pairs with tcgen05.mma.cta_group::2 on 256 x 256 tiles --
+// see its comment below; 1.07x cuBLAS over the Llama-3-8B projections (profiles/gemm_vs_cublas_r02_pair.json).
+// gemm_tc_kernel (n >= 2 with HI_GEMM_2CTA=0; 0.93x cuBLAS): persistent, warp-specialised, one CTA per SM.  Tile 128 (tokens) x 256 (out features)
 // x 64 (K), both operands TMA-loaded with SWIZZLE_128B into a 4-stage ring (48 KiB per stage); one thread issues
 // tcgen05.mma M128 N256 K16 (4 per stage) into a TMEM accumulator of 256 fp32 columns, double-buffered (512
 // columns), so the 4 epilogue warps drain tile i (tcgen05.ld -> + residual -> bf16 -> global) while the MMAs
