@@ -50,6 +50,8 @@ WORKLOADS = {
     "8B-1M": (32, 32, 8, 128, 1 << 20, 18944),
     "8B-128K": (32, 32, 8, 128, 131072, 18944),
     "tiny": (1, 4, 2, 64, 1024, 128),
+    # several layers and kv heads per rank at W = 2: the sharded parity must check layer 0, not the last layer
+    "small": (3, 16, 4, 128, 4096, 1024),
     # configs[3] / configs[4] are 8-GPU head-sharded workloads; on one GPU they run as one rank's share
     # (--emulate-shard 0/8): 1 kv head per layer.  70B: g = 8, so 9472 tokens x 8 rows = 2 full waves.
     "8B-4M": (32, 32, 8, 128, 4 << 20, 18944),
@@ -433,6 +435,8 @@ def run_ours(args, rank, world, local_rank, pg):
     barrier()
     sd1 = hi.stats()
     dec_sample = dout[0].clone() if model is None else None
+    if gdec is not None:   # the parity check is on layer 0: gather its decode output again (gdec holds the last layer's)
+        gather_heads(dout[0], group=pg, out=gdec)
     gdec_sample = gdec.clone() if gdec is not None else None
 
     # ---------------- e2e: the timed chunk again, inputs from pinned HOST memory --------------------------

@@ -104,3 +104,17 @@ def test_bench_two_ranks_self_launch():
     ps = res["parity_sample"]
     assert ps["ok"] and ps["qheads_checked"] == 4 and ps["gathered_prefill_rows"] > 0 and ps["gathered_decode_rows"] == 4
     assert res["value"] > 0 and res["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_multi_layer():
+    """Same launch on a 3-layer workload with 2 kv heads per rank: the gathered prefill AND decode rows of layer 0
+    must match the oracle (the decode gather buffer is overwritten by every layer, so the check re-gathers layer 0;
+    round 2 found it comparing the last layer's output against layer 0's oracle at 8B-128K)."""
+    res = run_bench("--workload", "small", "--steps", "2", "--warmup", "3", "--gpus", "2", "--ranks-share-gpu",
+                    "--no-cpu-baseline", timeout=900)
+    assert res["n_gpus"] == 2
+    ps = res["parity_sample"]
+    assert ps["ok"], ps
+    assert ps["qheads_checked"] == 16 and ps["gathered_decode_rows"] == 16
+    assert ps["decode_rel_l2_max"] <= ps["tol_rel_l2"]
