@@ -112,7 +112,7 @@ def test_bench_two_ranks_multi_layer():
     must match the oracle (the decode gather buffer is overwritten by every layer, so the check re-gathers layer 0;
     round 2 found it comparing the last layer's output against layer 0's oracle at 8B-128K)."""
     res = run_bench("--workload", "small", "--steps", "2", "--warmup", "3", "--gpus", "2", "--ranks-share-gpu",
-                    "--no-cpu-baseline", timeout=900)
+                    timeout=900)
     assert res["n_gpus"] == 2
     ps = res["parity_sample"]
     assert ps["ok"], ps
