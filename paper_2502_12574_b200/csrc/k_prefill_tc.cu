@@ -10,16 +10,17 @@
 // S >= 10K, §5), so both products run on the 5th-gen tensor cores:
 //
 //   S = Q K^T   tcgen05.mma kind::f16, A = Q tile (SMEM, K-major SW128), B = K tile (SMEM,
-//               K-major SW128), D = S in TMEM (fp32, 128 lanes x 128 cols, double-buffered)
-//   O += P V    A = P (bf16, SMEM, K-major SW128, written by the softmax warps),
+//               K-major SW128), D = S in TMEM (fp32, 128 lanes x 128 cols per Q tile)
+//   O += P V    A = P (bf16, in TMEM over the S columns, written by the softmax warps),
 //               B = V tile (SMEM, MN-major SW128), D = O in TMEM (fp32, 128 lanes x d cols)
 //
 // CTA = two 128-row Q tiles (GQA-packed: row r = t*g + j, loaded by one 3-D TMA box per 64
 // columns) sharing every K/V tile of 128 keys (halves the K/V SMEM/L2 traffic per FLOP).  Warps 0-3
 // own tile 0 and warps 4-7 tile 1 (softmax + O correction + epilogue; thread i owns TMEM lane /
-// row 32*(w%4)+i); warp 8: TMA producer; warp 9: TMEM allocator + single-thread MMA issuer.  P is
-// written back into the S columns of TMEM as packed bf16 and consumed from TMEM by the PV MMA
-// (A operand in TMEM), so P never touches shared memory; the MMA issuer alternates between the two
+// row 32*(w%4)+i); warp 8: TMA producer (K and V stages released on separate barriers); warp 9: TMEM
+// allocator + MMA issuer (the whole warp runs the issue loop, elect.sync issues).  P is written back into
+// the S columns of TMEM as packed bf16 in two 64-key halves, each consumed from TMEM by its part of the PV
+// MMA (A operand in TMEM), so P never touches shared memory; the MMA issuer alternates between the two
 // tiles, so one tile's softmax overlaps the other tile's QK^T / PV on the tensor core.
 // Online softmax in the log2 domain with lazy rescaling (the O correction is applied only when a
 // row max grows by more than 2^8), which is exact: O/l does not depend on the reference max.
