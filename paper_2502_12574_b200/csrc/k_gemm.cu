@@ -276,6 +276,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
                                     nb * P_GN + static_cast<int>(rank) * 128);
                 }
             }
+            // tail: the leader's multicast commits for the last stages must have landed in this CTA's barriers
+            // before it can exit (they fire asynchronously on MMA completion)
+            for (int j = it > P_STAGES ? it - P_STAGES : 0; j < it; ++j)
+                mbar_wait_cluster(empty(j % P_STAGES), (j / P_STAGES) & 1);
         }
     } else if (warp == 1) {
         if (leader) {   // ---------------- MMA issuer for the pair: the whole warp runs the loop, elect.sync issues
