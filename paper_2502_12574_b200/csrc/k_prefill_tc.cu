@@ -573,9 +573,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tc_fence_after();
                         issue_pv_half(tt, j, 1);
                         }
-                        if (j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));
                         if (HI_TWO_ISSUERS) HI_UCOMMIT(bar_ve2(tt, s));  // this tile is done with V(j)
                         else if (tt == last_v_tile(j)) HI_UCOMMIT(bar_ve(s));  // V(j) consumed by every tile
+                        // O final: the epilogue's only wait.  Issued after the stage release, so the last commit
+                        // of the CTA is one it waits for before exiting (commits are tracked in issue order)
+                        if (j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));
                         if (next) {
                             if (!have_k) { MMA_WAIT(bar_k((j + 1) % NS), ((j + 1) / NS) & 1); have_k = true; }
                             tc_fence_after();
