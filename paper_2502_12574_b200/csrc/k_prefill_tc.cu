@@ -142,8 +142,11 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 #define HI_TILE_MIX 0
 #endif
 static_assert(!HI_TILE_MIX || HI_SOFTMAX_SPLIT == 1, "tile mix: one softmax warp per row quarter");
+// HI_O_COMMIT_FIRST=1 (default): the final O commit precedes the last stage release.  The reverse order (=0, the
+// CTA's last commit is the one its epilogue waits for) measured 1.3 % slower per clock (748 vs 759, job AZ); the
+// stage-release arrival tracks the same MMAs and lands while the epilogue drains O (thousands of cycles)
 #ifndef HI_O_COMMIT_FIRST
-#define HI_O_COMMIT_FIRST 0   // A/B: commit the final O before the last stage release (round-2 order until late)
+#define HI_O_COMMIT_FIRST 1
 #endif
 // HI_KV_JOINT=1 (A/B only): the producer loads K(i) only once V(i - NS) is released too, in K(i), V(i) order -- the
 // round-1 prefetch distance (one tile step for K) with the separate barriers
@@ -579,8 +582,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (HI_O_COMMIT_FIRST && j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));  // A/B: the old order
                         if (HI_TWO_ISSUERS) HI_UCOMMIT(bar_ve2(tt, s));  // this tile is done with V(j)
                         else if (tt == last_v_tile(j)) HI_UCOMMIT(bar_ve(s));  // V(j) consumed by every tile
-                        // O final: the epilogue's only wait.  Issued after the stage release, so the last commit
-                        // of the CTA is one it waits for before exiting (commits are tracked in issue order)
+                        // O final (HI_O_COMMIT_FIRST=0 order): the epilogue's only wait
                         if (!HI_O_COMMIT_FIRST && j + 1 == nk_t[tt]) HI_UCOMMIT(bar_o(tt));
                         if (next) {
                             if (!have_k) { MMA_WAIT(bar_k((j + 1) % NS), ((j + 1) / NS) & 1); have_k = true; }
