@@ -41,6 +41,7 @@
 //   HI_TWO_ISSUERS=0     one MMA issuer warp                                 (one per tile: 523)
 //   HI_DESC_LO=0         64-bit descriptors                                  (low words: 743)
 //   HI_TILE_MIX=0        tile 1 = warps 4-7 (wins issue arbitration on every SMSP)  (interleaved: 744)
+//   HI_O_COMMIT_FIRST=1  final O commit before the last stage release        (after it: 748 vs 759)
 //   HI_MMA_SPIN=0, HI_WAIT_HINT(_MMA)=0: try_wait without a suspend hint     (polling: 711; 2 us hint on the MMA warp: -5 %)
 //   HI_FAKE_SOFTMAX / HI_FAKE_MAX / HI_SKIP_S / HI_SKIP_PV: timing-only (wrong results), never in the product
 //   HI_TRACE: CTA-0 clock64() timeline (hi_debug_prefill_trace), tools/trace_prefill.py
